@@ -1,0 +1,183 @@
+/*
+ * clothsim_b200.h -- C ABI of the B200-native cloth step.
+ *
+ * Replaces the per-frame hot path of the reference package `clothsim`
+ * (arxiv 2507.11794; /root/reference/pkg/src/clothsim):
+ *
+ *   cs_create       <- gpu/engine.py:111-147  Engine.__init__ (+ _allocate
+ *                      :151-191, _upload_static :193-244, params :246-285)
+ *   cs_step         <- gpu/engine.py:304-344  Engine.step (passes of
+ *                      gpu/kernels.py:81-339: zero_forces, spring_force,
+ *                      integrate, detect_cloth_edges, detect_obstacle_edges,
+ *                      respond, normal_update)
+ *   cs_run_pass     <- the individual dispatches of engine.py:313-339
+ *                      (debug snapshots, engine.py:315-337)
+ *   cs_respond      <- gpu/engine.py:346-352  Engine.run_respond_pass
+ *   cs_read         <- gpu/engine.py:362-378  read_positions / read_velocities /
+ *                      read_normals / read_forces_raw / read_accumulator_raw /
+ *                      read_counts
+ *   cs_write        <- writes through Engine.buffers.pos/.vel (test hooks,
+ *                      test_gpu_engine.py:99,201), set_external_accel
+ *                      (engine.py:297-302), inject_response (engine.py:354-358)
+ *   cs_frame_stats  <- StepResult.hits / .responded (engine.py:100-105)
+ *   cs_last_error   <- the reference's exception text
+ *
+ * All arguments are plain pointers and sizes.  Arrays passed to cs_create,
+ * cs_write and cs_read are HOST arrays (row-major (N,3) float32 etc., the
+ * reference's own buffer layouts); the library owns every device buffer.
+ * One handle = one CUDA stream; calls on a handle are not thread-safe, as in
+ * the reference.  Every function returns 0 on success or a
+ * negative CS_E* code; cs_last_error() returns the message.
+ */
+#ifndef CLOTHSIM_B200_H
+#define CLOTHSIM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CS_ABI_VERSION 1
+
+/* error codes (map to the reference's exception types) */
+#define CS_OK 0
+#define CS_E_INVALID (-1)      /* ValueError */
+#define CS_E_CAPACITY (-2)     /* gpu/layout.py CapacityError */
+#define CS_E_BUDGET (-3)       /* collision.py CollisionBudgetError */
+#define CS_E_NODEVICE (-4)     /* gpu/device.py AdapterUnavailable */
+#define CS_E_CUDA (-5)         /* CUDA runtime error */
+
+/* cs_desc.flags */
+#define CS_FLAG_EXPLICIT_EULER 1u   /* engine.py:45 FLAG_EXPLICIT_EULER */
+#define CS_FLAG_AVERAGE_RESPONSE 2u /* engine.py:46 FLAG_AVERAGE_RESPONSE */
+#define CS_FLAG_FIXED_POINT 4u      /* reference-engine arithmetic: per-spring
+                                       f32 forces accumulated as i32 at
+                                       fixed_point_scale (kernels.py:86-110),
+                                       bit-exact with the reference engine */
+#define CS_FLAG_FP64 8u             /* float64 state and arithmetic (float
+                                       gather only) */
+#define CS_FLAG_NO_GRAPH 16u        /* launch passes eagerly instead of
+                                       replaying a captured CUDA graph */
+#define CS_FLAG_FORCE_CSR 32u       /* use the generic per-node CSR gather even
+                                       when the topology is a regular grid */
+
+typedef struct cs_engine cs_engine;
+
+typedef struct cs_desc {
+    int32_t abi_version;       /* = CS_ABI_VERSION */
+    uint32_t flags;
+    /* grid topology: nx, ny > 0 selects the regular-grid stencil path, whose
+       spring/triangle/edge order must be generate_cloth_grid's
+       (mesh.py:223-317); grid_rest[6] are the single f32 rest lengths of
+       (structural +i, structural +j, shear (1,1), shear (-1,1), bend +2i,
+       bend +2j).  nx = ny = 0 selects the generic CSR path. */
+    int32_t nx, ny;
+    float grid_rest[6];
+    int64_t num_nodes;
+    /* springs (generic path; also used to build the CSR): (S,2) i32 endpoint
+       pairs, (S,) i32 kinds, (S,) f32 rest lengths -- engine.py:204-213 */
+    int64_t num_springs;
+    const int32_t *springs;
+    const int32_t *spring_kinds;
+    const float *spring_rest;
+    /* render triangulation (C,3) i32 and unique edges (E,2) i32 */
+    int64_t num_tris;
+    const int32_t *tris;
+    int64_t num_edges;
+    const int32_t *edges;
+    /* initial state (N,3) f32 positions (construction pose) and (N,) f32
+       inverse masses (0 = pinned) -- engine.py:199-202 */
+    const float *positions;
+    const double *positions64; /* optional, used by CS_FLAG_FP64 */
+    const float *inv_mass;
+    /* float64 solver-exact path (CS_FLAG_FP64): (N,) f64 masses, (N,) u8
+       pinned flags and (S,) f64 rest lengths, as in solver.py:86-172 */
+    const double *masses64;
+    const uint8_t *pinned;
+    const double *spring_rest64;
+    /* obstacle: (T,3,3) f32 corners and (T,3) f32 unit face normals
+       (engine.py:218-230) */
+    int64_t num_obstacle_tris;
+    const float *obstacle_corners;
+    const float *obstacle_normals;
+    /* SimParams (mesh.py:152-204) */
+    double dt;                 /* per substep: params.dt / params.substeps */
+    double gravity[3];
+    double stiffness[3];       /* structural, shear, bend */
+    double damping;
+    float epsilon_mt;
+    float response_margin;
+    int32_t fixed_point_scale;
+    int32_t substeps;
+    /* broad phase: uniform grid cell edge; <= 0 picks one automatically */
+    float cell_size;
+    /* CUDA stream to launch on (cudaStream_t); NULL = the library creates
+       its own non-blocking stream */
+    void *stream;
+} cs_desc;
+
+typedef struct cs_stats {
+    int64_t hits;          /* edge-triangle hits of the last frame */
+    int64_t responded;     /* nodes moved by the last respond pass */
+    int64_t frames;        /* frames stepped since creation */
+    int64_t hit_counter;   /* cumulative hitCounter buffer value */
+} cs_stats;
+
+/* buffer ids for cs_read / cs_write */
+#define CS_BUF_POSITIONS 0      /* f32 (N,3) (f64 with CS_FLAG_FP64 via _64) */
+#define CS_BUF_VELOCITIES 1
+#define CS_BUF_NORMALS 2
+#define CS_BUF_PREV_POSITIONS 3
+#define CS_BUF_FORCES_RAW 4     /* i32 (N,3) spring-only fixed-point forces of
+                                   the last spring_force pass */
+#define CS_BUF_ACCUMULATOR 5    /* i32 (N,3) responseAccumulator */
+#define CS_BUF_COUNTS 6         /* i32 (N,)  responseCount */
+#define CS_BUF_EXT_ACCEL 7      /* f32 (N,3) externalAccel (write only) */
+#define CS_BUF_POSITIONS64 8    /* f64 (N,3) (CS_FLAG_FP64 engines) */
+#define CS_BUF_VELOCITIES64 9
+
+/* passes for cs_run_pass (engine.py:313-339) */
+#define CS_PASS_FORCE_INTEGRATE 0 /* zero_forces + spring_force + integrate */
+#define CS_PASS_DETECT 1          /* detect_cloth_edges + detect_obstacle_edges */
+#define CS_PASS_RESPOND 2
+#define CS_PASS_NORMALS 3
+
+int cs_create(const cs_desc *desc, cs_engine **out);
+int cs_destroy(cs_engine *h);
+/* Advance `frames` whole frames (asynchronous on the engine's stream). */
+int cs_step(cs_engine *h, int32_t frames);
+int cs_run_pass(cs_engine *h, int32_t pass_id);
+/* Respond pass alone; writes the responded count (synchronises). */
+int cs_respond(cs_engine *h, int64_t *responded);
+/* Synchronise and report the last frame's hit / respond counts. */
+int cs_frame_stats(cs_engine *h, cs_stats *out);
+/* Hits / responded of frame `frame` (0-based), kept on device in a ring of
+   the last 4096 frames so a step never has to synchronise (engine.py:100-105
+   StepResult fields, resolved lazily). */
+int cs_frame_hits(cs_engine *h, int64_t frame, int64_t *hits, int64_t *responded);
+int cs_read(cs_engine *h, int32_t buffer_id, void *host_dst);
+int cs_write(cs_engine *h, int32_t buffer_id, const void *host_src);
+/* Single node accumulator write (engine.py:354-358 inject_response). */
+int cs_inject_response(cs_engine *h, int64_t node, const int32_t raw[3], int32_t count);
+int cs_synchronize(cs_engine *h);
+/* Device pointer of a state plane for halo exchange / zero-copy interop:
+   which = 0..5 -> x, y, z, vx, vy, vz of the CURRENT state; returns the
+   pitch (elements per grid row) through *pitch. */
+int cs_state_plane(cs_engine *h, int32_t which, void **dev_ptr, int64_t *pitch);
+/* Number of kernels one cs_step(h, 1) launches. */
+int cs_kernels_per_frame(cs_engine *h, int32_t *count);
+/* Broad-phase statistics: cells, references, last frame's candidate pairs. */
+int cs_broadphase_stats(cs_engine *h, int64_t out[4]);
+/* Number of visible CUDA devices (0 when no driver / device): the adapter
+   probe of gpu/device.py:156-172 get_adapter. */
+int cs_device_count(void);
+/* Free / total device memory, for the capacity check (gpu/layout.py:192-202). */
+int cs_mem_info(int64_t *free_bytes, int64_t *total_bytes);
+const char *cs_last_error(void);
+int cs_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CLOTHSIM_B200_H */

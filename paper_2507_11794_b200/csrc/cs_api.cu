@@ -1,0 +1,833 @@
+// cs_api.cu -- the C ABI (include/clothsim_b200.h): engine construction,
+// frame sequencing and CUDA-graph replay, host <-> device transfers.
+//
+// Mirrors gpu/engine.py:108-394 (Engine): construction bakes the cloth and
+// obstacle into device buffers (engine.py:193-244), a frame submits
+//   [spring_force+integrate] x substeps -> detect A -> detect B -> respond
+//   -> normals                                           (engine.py:304-344)
+// and readbacks return copies in the reference's (N,3) layouts.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/clothsim_b200.h"
+#include "cs_collide.cuh"
+#include "cs_common.cuh"
+#include "cs_kernels.cuh"
+
+
+using namespace cs;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                      \
+    do {                                                                              \
+        cudaError_t e_ = (call);                                                      \
+        if (e_ != cudaSuccess)                                                        \
+            return fail(CS_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <typename T>
+static cudaError_t dalloc(T **p, size_t count) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    return cudaMalloc((void **)p, count * sizeof(T));
+}
+
+struct cs_engine {
+    uint32_t flags = 0;
+    bool grid = false, fixed = false, fp64 = false, use_graph = true;
+    int64_t N = 0, nx = 0, rows = 0, pitch = 0, plane = 0;
+    cudaStream_t st = nullptr;
+    bool own_stream = false;
+    int num_sms = 148;
+    int substeps = 1;
+    bool average = true;
+
+    void *state[2] = {nullptr, nullptr};
+    int cur = 0;
+    size_t esz = 4;
+    void *normals = nullptr;
+    uint32_t *pinbits = nullptr;
+    float *inv_mass = nullptr;     // CSR f32 path
+    double *mass64 = nullptr;      // f64 path
+    uint8_t *pinned8 = nullptr;
+    void *ext = nullptr;
+    bool has_ext = false;
+    int32_t *forces_raw = nullptr;
+    bool forces_valid = false;
+
+    int64_t *csr_off = nullptr;
+    int32_t *csr_nbr = nullptr;
+    uint8_t *csr_kind = nullptr;
+    float *csr_rest = nullptr;
+    double *csr_rest64 = nullptr;
+    int64_t *inc_off = nullptr;
+    int32_t *inc_tri = nullptr;
+    void *face = nullptr;
+    int32_t *tris_g = nullptr;     // triangles in storage indices
+    int32_t *edges_g = nullptr;
+    int64_t nc = 0, ne = 0, nt = 0;
+
+    bool has_obstacle = false;
+    float *corners = nullptr, *onormals = nullptr;
+    BroadPhase bp;
+    int32_t *acc = nullptr, *count = nullptr;
+    uint32_t *touched = nullptr, *touched_n = nullptr;
+    // [frame_hits, frame_responded, hit_counter, frame_counter, ring (2 x kRing)]
+    unsigned long long *stats = nullptr;
+    static constexpr int kRing = 4096;
+    float eps = 1e-6f, margin = 1e-3f;
+
+    void *stage = nullptr;
+    size_t stage_bytes = 0;
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    int64_t frames = 0;
+    StepParams sp{};
+    CsrParams cp{};
+
+    int64_t gidx(int64_t n) const { return grid ? (n / nx) * pitch + (n % nx) : n; }
+    CollideArgs cargs() const {
+        CollideArgs A;
+        A.pos = (const float *)state[cur];
+        A.plane = plane;
+        A.acc = acc;
+        A.count = count;
+        A.touched = touched;
+        A.touched_n = touched_n;
+        A.frame_hits = stats;
+        A.frame_responded = stats + 1;
+        A.hit_counter = stats + 2;
+        A.frame_counter = stats + 3;
+        A.ring = stats + 4;
+        A.ring_size = kRing;
+        A.eps = eps;
+        A.margin = margin;
+        A.pad = 1e-5f;  // kernels.py:48 BOX_PAD
+        A.scale_f = sp.scale_f;
+        A.scale_d = sp.scale_d;
+        return A;
+    }
+    int kernels_per_frame() const {
+        int k = substeps;  // one fused force+integrate launch per substep
+        if (has_obstacle) k += 2 /*detect*/ + 2 /*respond + frame_end*/;
+        k += grid ? 1 : 2;  // normals
+        return k;
+    }
+};
+
+// ---------------------------------------------------------------------------
+// layout transposes: host AoS (N,3) <-> device SoA planes (pitch layout)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_aos_to_planes(int64_t N, int64_t nx, int64_t pitch, int64_t plane, int comps,
+                                const T *__restrict__ aos, T *__restrict__ planes) {
+    const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    const int64_t g = (n / nx) * pitch + (n % nx);
+    for (int c = 0; c < comps; ++c) planes[c * plane + g] = aos[n * comps + c];
+}
+template <typename T>
+__global__ void k_planes_to_aos(int64_t N, int64_t nx, int64_t pitch, int64_t plane, int comps,
+                                const T *__restrict__ planes, T *__restrict__ aos) {
+    const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    const int64_t g = (n / nx) * pitch + (n % nx);
+    for (int c = 0; c < comps; ++c) aos[n * comps + c] = planes[c * plane + g];
+}
+__global__ void k_f64_to_f32(int64_t n, const double *a, float *b) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) b[i] = (float)a[i];
+}
+__global__ void k_f32_to_f64(int64_t n, const float *a, double *b) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) b[i] = (double)a[i];
+}
+static inline unsigned nb(int64_t n) { return (unsigned)((n + 255) / 256); }
+
+static int ensure_stage(cs_engine *h, size_t bytes) {
+    if (bytes > h->stage_bytes) {
+        if (h->stage) cudaFree(h->stage);
+        CK(cudaMalloc(&h->stage, bytes));
+        h->stage_bytes = bytes;
+    }
+    return 0;
+}
+
+// upload host AoS into planes (T = float / double / int32)
+template <typename T>
+static int upload_planes(cs_engine *h, const T *host, T *planes, int comps) {
+    const size_t bytes = (size_t)h->N * comps * sizeof(T);
+    if (int r = ensure_stage(h, bytes)) return r;
+    CK(cudaMemcpyAsync(h->stage, host, bytes, cudaMemcpyHostToDevice, h->st));
+    const int64_t nxx = h->grid ? h->nx : h->N;
+    k_aos_to_planes<T><<<nb(h->N), 256, 0, h->st>>>(h->N, nxx, h->pitch, h->plane, comps,
+                                                    (const T *)h->stage, planes);
+    CK(cudaGetLastError());
+    return 0;
+}
+template <typename T>
+static int download_planes(cs_engine *h, const T *planes, T *host, int comps) {
+    const size_t bytes = (size_t)h->N * comps * sizeof(T);
+    if (int r = ensure_stage(h, bytes)) return r;
+    const int64_t nxx = h->grid ? h->nx : h->N;
+    k_planes_to_aos<T><<<nb(h->N), 256, 0, h->st>>>(h->N, nxx, h->pitch, h->plane, comps, planes,
+                                                    (T *)h->stage);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(host, h->stage, bytes, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    return 0;
+}
+
+static void drop_graphs(cs_engine *h) {
+    for (int i = 0; i < 2; ++i)
+        if (h->graph[i]) {
+            cudaGraphExecDestroy(h->graph[i]);
+            h->graph[i] = nullptr;
+        }
+}
+
+// ---------------------------------------------------------------------------
+// passes
+// ---------------------------------------------------------------------------
+static void pass_force_integrate(cs_engine *h) {
+    for (int s = 0; s < h->substeps; ++s) {
+        const int src = h->cur, dst = 1 - h->cur;
+        if (h->fp64) {
+            launch_csr_step_f64(h->cp, (const double *)h->state[src], (double *)h->state[dst],
+                                h->csr_off, h->csr_nbr, h->csr_kind, h->csr_rest64, h->mass64,
+                                h->pinned8, h->has_ext ? (const double *)h->ext : nullptr, h->st);
+        } else if (h->grid) {
+            launch_grid_step(h->sp, h->fixed, (const float *)h->state[src], (float *)h->state[dst],
+                             h->pinbits, h->has_ext ? (const float *)h->ext : nullptr, h->st);
+        } else {
+            launch_csr_step(h->cp, h->fixed, (const float *)h->state[src], (float *)h->state[dst],
+                            h->csr_off, h->csr_nbr, h->csr_kind, h->csr_rest, h->inv_mass,
+                            h->has_ext ? (const float *)h->ext : nullptr, h->st);
+        }
+        h->cur = dst;
+    }
+    h->forces_valid = true;
+}
+
+static void pass_detect(cs_engine *h) {
+    cudaMemsetAsync(h->stats, 0, 2 * sizeof(unsigned long long), h->st);
+    if (!h->has_obstacle) return;
+    launch_detect(h->cargs(), h->bp, h->corners, h->onormals, h->edges_g, h->ne, h->tris_g, h->nc,
+                  h->st);
+}
+
+static void pass_respond(cs_engine *h) {
+    if (!h->has_obstacle) return;
+    launch_respond(h->cargs(), (float *)h->state[h->cur], h->grid ? h->pinbits : nullptr,
+                   h->grid ? nullptr : h->inv_mass, h->average ? 1 : 0, h->N, h->num_sms,
+                   /*end_of_frame=*/true, h->st);
+}
+
+static void pass_normals(cs_engine *h) {
+    if (h->fp64) {
+        launch_csr_normals_f64(h->N, h->plane, h->nc, (const double *)h->state[h->cur], h->tris_g,
+                               (double *)h->face, h->inc_off, h->inc_tri, (double *)h->normals, h->st);
+    } else if (h->grid) {
+        launch_grid_normals(h->sp, h->fixed, (const float *)h->state[h->cur], (float *)h->normals, h->st);
+    } else {
+        launch_csr_normals(h->N, h->plane, h->nc, h->fixed, (const float *)h->state[h->cur],
+                           h->tris_g, (float *)h->face, h->inc_off, h->inc_tri, (float *)h->normals,
+                           h->st);
+    }
+}
+
+static void launch_frame(cs_engine *h) {
+    pass_force_integrate(h);
+    if (h->has_obstacle) {
+        pass_detect(h);
+        pass_respond(h);
+    }
+    pass_normals(h);
+}
+
+// ---------------------------------------------------------------------------
+// construction
+// ---------------------------------------------------------------------------
+extern "C" int cs_abi_version(void) { return CS_ABI_VERSION; }
+extern "C" const char *cs_last_error(void) { return g_err.c_str(); }
+
+static int build(cs_engine *h, const cs_desc *d) {
+    const int64_t N = d->num_nodes;
+    h->flags = d->flags;
+    h->fixed = (d->flags & CS_FLAG_FIXED_POINT) != 0;
+    h->fp64 = (d->flags & CS_FLAG_FP64) != 0;
+    h->use_graph = (d->flags & CS_FLAG_NO_GRAPH) == 0;
+    h->average = (d->flags & CS_FLAG_AVERAGE_RESPONSE) != 0;
+    h->substeps = d->substeps < 1 ? 1 : d->substeps;
+    h->N = N;
+    if (h->fp64 && h->fixed) return fail(CS_E_INVALID, "CS_FLAG_FP64 and CS_FLAG_FIXED_POINT are exclusive");
+    if (h->fp64 && d->num_obstacle_tris > 0)
+        return fail(CS_E_INVALID, "float64 engines do not support obstacles yet");
+    if (h->fp64 && (!d->masses64 || !d->pinned || !d->spring_rest64))
+        return fail(CS_E_INVALID, "float64 engines need masses64, pinned and spring_rest64");
+
+    // uniform inverse mass among free nodes => grid stencil eligible
+    float im_free = 0.f;
+    bool uniform = true;
+    for (int64_t i = 0; i < N; ++i) {
+        const float v = d->inv_mass[i];
+        if (v > 0.f) {
+            if (im_free == 0.f) im_free = v;
+            else if (v != im_free) { uniform = false; break; }
+        }
+    }
+    h->grid = d->nx >= 2 && d->ny >= 2 && (int64_t)d->nx * d->ny == N && !h->fp64 && uniform &&
+              !(d->flags & CS_FLAG_FORCE_CSR);
+    h->esz = h->fp64 ? 8 : 4;
+    if (h->grid) {
+        h->nx = d->nx;
+        h->rows = d->ny;
+        h->pitch = (d->nx + 31) / 32 * 32;
+        h->plane = h->pitch * h->rows;
+    } else {
+        h->nx = N;
+        h->rows = 1;
+        h->pitch = N;
+        h->plane = N;
+    }
+    const int64_t P = h->plane;
+
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (d->stream) {
+        h->st = (cudaStream_t)d->stream;
+    } else {
+        CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+        h->own_stream = true;
+    }
+
+    // ---- parameters (engine.py:246-285) ----
+    StepParams &sp = h->sp;
+    sp.nx = (int)h->nx;
+    sp.ny = (int)h->rows;
+    sp.pitch = (int)h->pitch;
+    sp.plane = P;
+    sp.dt = (float)d->dt;
+    sp.gx = (float)d->gravity[0];
+    sp.gy = (float)d->gravity[1];
+    sp.gz = (float)d->gravity[2];
+    sp.k_struct = (float)d->stiffness[0];
+    sp.k_shear = (float)d->stiffness[1];
+    sp.k_bend = (float)d->stiffness[2];
+    sp.damping = (float)d->damping;
+    for (int q = 0; q < 6; ++q) sp.rest[q] = d->grid_rest[q];
+    sp.inv_mass = im_free;
+    sp.scale_f = (float)d->fixed_point_scale;
+    sp.scale_d = (double)d->fixed_point_scale;
+    sp.explicit_euler = (d->flags & CS_FLAG_EXPLICIT_EULER) ? 1 : 0;
+    CsrParams &cp = h->cp;
+    cp.n = N;
+    cp.plane = P;
+    cp.dt = sp.dt;
+    cp.gx = sp.gx; cp.gy = sp.gy; cp.gz = sp.gz;
+    cp.damping = sp.damping;
+    cp.scale_f = sp.scale_f;
+    cp.scale_d = sp.scale_d;
+    cp.k[0] = sp.k_struct; cp.k[1] = sp.k_shear; cp.k[2] = sp.k_bend;
+    cp.dt_d = d->dt;
+    for (int q = 0; q < 3; ++q) {
+        cp.g_d[q] = d->gravity[q];
+        cp.k_d[q] = d->stiffness[q];
+    }
+    cp.damping_d = d->damping;
+    cp.explicit_euler = sp.explicit_euler;
+    h->eps = d->epsilon_mt;
+    h->margin = d->response_margin;
+
+    // ---- state (ping-pong SoA planes) ----
+    for (int b = 0; b < 2; ++b) {
+        CK(cudaMalloc(&h->state[b], 6 * P * h->esz));
+        CK(cudaMemsetAsync(h->state[b], 0, 6 * P * h->esz, h->st));
+    }
+    CK(cudaMalloc(&h->normals, 3 * P * h->esz));
+    CK(cudaMemsetAsync(h->normals, 0, 3 * P * h->esz, h->st));
+    if (h->fp64) {
+        if (d->positions64) {
+            if (int r = upload_planes<double>(h, d->positions64, (double *)h->state[0], 3)) return r;
+        } else {
+            if (int r = upload_planes<float>(h, d->positions, (float *)h->state[1], 3)) return r;
+            k_f32_to_f64<<<nb(3 * P), 256, 0, h->st>>>(3 * P, (const float *)h->state[1], (double *)h->state[0]);
+        }
+    } else {
+        if (int r = upload_planes<float>(h, d->positions, (float *)h->state[0], 3)) return r;
+    }
+    CK(cudaMemcpyAsync(h->state[1], h->state[0], 6 * P * h->esz, cudaMemcpyDeviceToDevice, h->st));
+
+    // ---- masses / pins ----
+    if (h->grid) {
+        const int64_t words = (P + 31) / 32;
+        std::vector<uint32_t> bits(words, 0u);
+        for (int64_t n = 0; n < N; ++n)
+            if (!(d->inv_mass[n] > 0.f)) {
+                const int64_t g = h->gidx(n);
+                bits[g >> 5] |= 1u << (g & 31);
+            }
+        CK(dalloc(&h->pinbits, words));
+        CK(cudaMemcpyAsync(h->pinbits, bits.data(), words * 4, cudaMemcpyHostToDevice, h->st));
+    }
+    CK(dalloc(&h->inv_mass, P));  // storage layout (the respond pass reads it too)
+    CK(cudaMemsetAsync(h->inv_mass, 0, P * 4, h->st));
+    if (int r = upload_planes<float>(h, d->inv_mass, h->inv_mass, 1)) return r;
+    if (h->fp64) {
+        CK(dalloc(&h->mass64, N));
+        CK(dalloc(&h->pinned8, N));
+        CK(cudaMemcpyAsync(h->mass64, d->masses64, N * 8, cudaMemcpyHostToDevice, h->st));
+        CK(cudaMemcpyAsync(h->pinned8, d->pinned, N, cudaMemcpyHostToDevice, h->st));
+    }
+
+    // ---- spring CSR (generic / f64 paths): ascending spring id per node ----
+    if (!h->grid) {
+        const int64_t S = d->num_springs;
+        std::vector<int64_t> off(N + 1, 0);
+        for (int64_t s = 0; s < S; ++s) {
+            const int32_t a = d->springs[2 * s], b = d->springs[2 * s + 1];
+            if (a < 0 || a >= N || b < 0 || b >= N) return fail(CS_E_INVALID, "spring endpoint out of range");
+            off[a + 1]++;
+            off[b + 1]++;
+        }
+        for (int64_t i = 0; i < N; ++i) off[i + 1] += off[i];
+        std::vector<int64_t> fill(off.begin(), off.end() - 1);
+        std::vector<int32_t> nbr(2 * S);
+        std::vector<uint8_t> kind(2 * S);
+        std::vector<float> rest(2 * S);
+        std::vector<double> rest64(h->fp64 ? 2 * S : 0);
+        for (int64_t s = 0; s < S; ++s) {  // s ascending => each list sorted by spring id
+            const int32_t a = d->springs[2 * s], b = d->springs[2 * s + 1];
+            const int k = d->spring_kinds[s];
+            if (k < 0 || k > 2) return fail(CS_E_INVALID, "spring kind must be 0, 1 or 2");
+            int64_t ea = fill[a]++, eb = fill[b]++;
+            nbr[ea] = b; nbr[eb] = a;
+            kind[ea] = kind[eb] = (uint8_t)k;
+            rest[ea] = rest[eb] = d->spring_rest[s];
+            if (h->fp64) rest64[ea] = rest64[eb] = d->spring_rest64[s];
+        }
+        CK(dalloc(&h->csr_off, N + 1));
+        CK(dalloc(&h->csr_nbr, 2 * S));
+        CK(dalloc(&h->csr_kind, 2 * S));
+        CK(dalloc(&h->csr_rest, 2 * S));
+        CK(cudaMemcpy(h->csr_off, off.data(), (N + 1) * 8, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->csr_nbr, nbr.data(), 2 * S * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->csr_kind, kind.data(), 2 * S, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->csr_rest, rest.data(), 2 * S * 4, cudaMemcpyHostToDevice));
+        if (h->fp64) {
+            CK(dalloc(&h->csr_rest64, 2 * S));
+            CK(cudaMemcpy(h->csr_rest64, rest64.data(), 2 * S * 8, cudaMemcpyHostToDevice));
+        }
+    }
+
+    // ---- triangles, incidence CSR, edges ----
+    h->nc = d->num_tris;
+    h->ne = d->num_edges;
+    {
+        const int64_t C = h->nc;
+        std::vector<int32_t> tg(3 * C);
+        for (int64_t i = 0; i < 3 * C; ++i) {
+            const int32_t v = d->tris[i];
+            if (v < 0 || v >= N) return fail(CS_E_INVALID, "triangle vertex out of range");
+            tg[i] = (int32_t)h->gidx(v);
+        }
+        CK(dalloc(&h->tris_g, 3 * C));
+        CK(cudaMemcpy(h->tris_g, tg.data(), 3 * C * 4, cudaMemcpyHostToDevice));
+        if (!h->grid) {
+            // engine.py:232-242: ascending triangle order per node; the f64
+            // path uses np.add.at's (corner, triangle) order (mesh.py:425-427)
+            std::vector<int64_t> off(N + 1, 0);
+            for (int64_t i = 0; i < 3 * C; ++i) off[d->tris[i] + 1]++;
+            for (int64_t i = 0; i < N; ++i) off[i + 1] += off[i];
+            std::vector<int64_t> fill(off.begin(), off.end() - 1);
+            std::vector<int32_t> inc(3 * C);
+            if (h->fp64) {
+                for (int c = 0; c < 3; ++c)
+                    for (int64_t t = 0; t < C; ++t) inc[fill[d->tris[3 * t + c]]++] = (int32_t)t;
+            } else {
+                for (int64_t t = 0; t < C; ++t)
+                    for (int c = 0; c < 3; ++c) {
+                        const int32_t v = d->tris[3 * t + c];
+                        // a triangle listing a vertex twice appears twice, like reduceat
+                        inc[fill[v]++] = (int32_t)t;
+                    }
+            }
+            CK(dalloc(&h->inc_off, N + 1));
+            CK(dalloc(&h->inc_tri, 3 * C));
+            CK(cudaMemcpy(h->inc_off, off.data(), (N + 1) * 8, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(h->inc_tri, inc.data(), 3 * C * 4, cudaMemcpyHostToDevice));
+            CK(cudaMalloc(&h->face, 3 * (C > 0 ? C : 1) * h->esz));
+        }
+        if (h->ne > 0) {
+            std::vector<int32_t> eg(2 * h->ne);
+            for (int64_t i = 0; i < 2 * h->ne; ++i) {
+                const int32_t v = d->edges[i];
+                if (v < 0 || v >= N) return fail(CS_E_INVALID, "edge vertex out of range");
+                eg[i] = (int32_t)h->gidx(v);
+            }
+            CK(dalloc(&h->edges_g, 2 * h->ne));
+            CK(cudaMemcpy(h->edges_g, eg.data(), 2 * h->ne * 4, cudaMemcpyHostToDevice));
+        }
+    }
+
+    // ---- collision buffers + broad phase (engine.py:218-230) ----
+    CK(dalloc(&h->stats, 4 + 2 * cs_engine::kRing));
+    CK(cudaMemsetAsync(h->stats, 0, (4 + 2 * cs_engine::kRing) * sizeof(unsigned long long), h->st));
+    CK(dalloc(&h->acc, 3 * P));
+    CK(dalloc(&h->count, P));
+    CK(dalloc(&h->touched, P));
+    CK(dalloc(&h->touched_n, 1));
+    CK(cudaMemsetAsync(h->acc, 0, 3 * P * 4, h->st));
+    CK(cudaMemsetAsync(h->count, 0, P * 4, h->st));
+    CK(cudaMemsetAsync(h->touched_n, 0, 4, h->st));
+    h->nt = d->num_obstacle_tris;
+    h->has_obstacle = h->nt > 0;
+    if (h->has_obstacle) {
+        CK(dalloc(&h->corners, 9 * h->nt));
+        CK(dalloc(&h->onormals, 3 * h->nt));
+        CK(cudaMemcpy(h->corners, d->obstacle_corners, 9 * h->nt * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->onormals, d->obstacle_normals, 3 * h->nt * 4, cudaMemcpyHostToDevice));
+        if (build_broadphase(h->bp, h->corners, h->nt, d->obstacle_corners, d->cell_size, h->st))
+            return fail(CS_E_CUDA, std::string("broad-phase build failed: ") +
+                                       cudaGetErrorString(cudaGetLastError()));
+    }
+    CK(cudaStreamSynchronize(h->st));
+    CK(cudaGetLastError());
+    return 0;
+}
+
+extern "C" int cs_destroy(cs_engine *h) {
+    if (!h) return 0;
+    if (h->st) cudaStreamSynchronize(h->st);
+    drop_graphs(h);
+    void *ptrs[] = {h->state[0], h->state[1], h->normals, h->pinbits, h->inv_mass, h->mass64,
+                    h->pinned8, h->ext, h->forces_raw, h->csr_off, h->csr_nbr, h->csr_kind,
+                    h->csr_rest, h->csr_rest64, h->inc_off, h->inc_tri, h->face, h->tris_g,
+                    h->edges_g, h->corners, h->onormals, h->acc, h->count, h->touched,
+                    h->touched_n, h->stats, h->stage};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    if (h->has_obstacle) free_broadphase(h->bp);
+    if (h->own_stream && h->st) cudaStreamDestroy(h->st);
+    delete h;
+    return 0;
+}
+
+extern "C" int cs_create(const cs_desc *d, cs_engine **out) {
+    if (!d || !out) return fail(CS_E_INVALID, "null argument");
+    *out = nullptr;
+    if (d->abi_version != CS_ABI_VERSION) return fail(CS_E_INVALID, "ABI version mismatch");
+    if (d->num_nodes < 1 || !d->positions || !d->inv_mass)
+        return fail(CS_E_INVALID, "num_nodes, positions and inv_mass are required");
+    if (d->num_obstacle_tris > 0 && (!d->obstacle_corners || !d->obstacle_normals))
+        return fail(CS_E_INVALID, "obstacle arrays missing");
+    if (d->num_nodes > ((int64_t)1 << 31) - 1) return fail(CS_E_CAPACITY, "more than 2^31-1 nodes");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(CS_E_NODEVICE, "no CUDA device is available");
+    }
+    cs_engine *h = new cs_engine();
+    int r = build(h, d);
+    if (r) {
+        std::string keep = g_err;
+        cudaGetLastError();
+        cs_destroy(h);
+        g_err = keep;
+        return r;
+    }
+    *out = h;
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// stepping
+// ---------------------------------------------------------------------------
+extern "C" int cs_step(cs_engine *h, int32_t frames) {
+    if (!h) return fail(CS_E_INVALID, "null engine");
+    for (int32_t f = 0; f < frames; ++f) {
+        if (h->use_graph) {
+            const int start = h->cur;
+            if (!h->graph[start]) {
+                cudaGraph_t g;
+                CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
+                launch_frame(h);
+                CK(cudaStreamEndCapture(h->st, &g));
+                CK(cudaGraphInstantiate(&h->graph[start], g, 0));
+                cudaGraphDestroy(g);
+                h->cur = start;  // capture did not execute anything
+            }
+            CK(cudaGraphLaunch(h->graph[start], h->st));
+            // replay the parity bookkeeping of one frame
+            if (h->substeps & 1) h->cur = 1 - start;
+            h->forces_valid = true;
+        } else {
+            launch_frame(h);
+            CK(cudaGetLastError());
+        }
+        h->frames++;
+    }
+    return 0;
+}
+
+extern "C" int cs_run_pass(cs_engine *h, int32_t pass_id) {
+    if (!h) return fail(CS_E_INVALID, "null engine");
+    switch (pass_id) {
+        case CS_PASS_FORCE_INTEGRATE: pass_force_integrate(h); break;
+        case CS_PASS_DETECT: pass_detect(h); break;
+        case CS_PASS_RESPOND:
+            if (h->has_obstacle) pass_respond(h);
+            break;
+        case CS_PASS_NORMALS: pass_normals(h); h->frames++; break;
+        default: return fail(CS_E_INVALID, "unknown pass id");
+    }
+    CK(cudaGetLastError());
+    return 0;
+}
+
+extern "C" int cs_respond(cs_engine *h, int64_t *responded) {
+    if (!h) return fail(CS_E_INVALID, "null engine");
+    CK(cudaMemsetAsync(h->stats + 1, 0, sizeof(unsigned long long), h->st));
+    launch_respond(h->cargs(), (float *)h->state[h->cur], h->grid ? h->pinbits : nullptr,
+                   h->grid ? nullptr : h->inv_mass, h->average ? 1 : 0, h->N, h->num_sms,
+                   /*end_of_frame=*/false, h->st);
+    CK(cudaGetLastError());
+    unsigned long long v = 0;
+    CK(cudaMemcpyAsync(&v, h->stats + 1, sizeof(v), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    if (responded) *responded = (int64_t)v;
+    return 0;
+}
+
+extern "C" int cs_frame_stats(cs_engine *h, cs_stats *out) {
+    if (!h || !out) return fail(CS_E_INVALID, "null argument");
+    unsigned long long v[3] = {0, 0, 0};
+    CK(cudaMemcpyAsync(v, h->stats, sizeof(v), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    out->hits = (int64_t)v[0];
+    out->responded = (int64_t)v[1];
+    out->hit_counter = (int64_t)v[2];
+    out->frames = h->frames;
+    return 0;
+}
+
+extern "C" int cs_frame_hits(cs_engine *h, int64_t frame, int64_t *hits, int64_t *responded) {
+    if (!h) return fail(CS_E_INVALID, "null engine");
+    if (!h->has_obstacle) {
+        if (hits) *hits = 0;
+        if (responded) *responded = 0;
+        return 0;
+    }
+    unsigned long long fc = 0, v[2] = {0, 0};
+    CK(cudaMemcpyAsync(&fc, h->stats + 3, sizeof(fc), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    if (frame < 0 || (unsigned long long)frame >= fc ||
+        fc - (unsigned long long)frame > (unsigned long long)cs_engine::kRing)
+        return fail(CS_E_INVALID, "frame statistics no longer available (ring of 4096 frames)");
+    const int64_t slot = frame % cs_engine::kRing;
+    CK(cudaMemcpy(v, h->stats + 4 + 2 * slot, sizeof(v), cudaMemcpyDeviceToHost));
+    if (hits) *hits = (int64_t)v[0];
+    if (responded) *responded = (int64_t)v[1];
+    return 0;
+}
+
+extern "C" int cs_synchronize(cs_engine *h) {
+    if (!h) return fail(CS_E_INVALID, "null engine");
+    CK(cudaStreamSynchronize(h->st));
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// transfers
+// ---------------------------------------------------------------------------
+extern "C" int cs_read(cs_engine *h, int32_t id, void *dst) {
+    if (!h || !dst) return fail(CS_E_INVALID, "null argument");
+    const int64_t P = h->plane;
+    switch (id) {
+        case CS_BUF_POSITIONS:
+        case CS_BUF_VELOCITIES:
+        case CS_BUF_PREV_POSITIONS:
+        case CS_BUF_NORMALS: {
+            const void *base = id == CS_BUF_NORMALS ? h->normals
+                               : id == CS_BUF_PREV_POSITIONS ? h->state[1 - h->cur]
+                                                             : h->state[h->cur];
+            const int64_t o = id == CS_BUF_VELOCITIES ? 3 * P : 0;
+            if (h->fp64) {
+                float *tmp;
+                CK(cudaMalloc(&tmp, 3 * P * 4));
+                k_f64_to_f32<<<nb(3 * P), 256, 0, h->st>>>(3 * P, (const double *)base + o, tmp);
+                int r = download_planes<float>(h, tmp, (float *)dst, 3);
+                cudaFree(tmp);
+                return r;
+            }
+            return download_planes<float>(h, (const float *)base + o, (float *)dst, 3);
+        }
+        case CS_BUF_POSITIONS64:
+        case CS_BUF_VELOCITIES64: {
+            if (!h->fp64) return fail(CS_E_INVALID, "float64 buffers need a CS_FLAG_FP64 engine");
+            const int64_t o = id == CS_BUF_VELOCITIES64 ? 3 * P : 0;
+            return download_planes<double>(h, (const double *)h->state[h->cur] + o, (double *)dst, 3);
+        }
+        case CS_BUF_FORCES_RAW: {
+            if (h->fp64) return fail(CS_E_INVALID, "read_forces_raw is a float32-engine buffer");
+            if (!h->forces_valid) {
+                memset(dst, 0, (size_t)h->N * 3 * 4);
+                return 0;
+            }
+            if (!h->forces_raw) CK(dalloc(&h->forces_raw, 3 * P));
+            const float *prev = (const float *)h->state[1 - h->cur];
+            if (h->grid)
+                launch_grid_forces(h->sp, prev, h->forces_raw, h->st);
+            else
+                launch_csr_forces(h->cp, prev, h->csr_off, h->csr_nbr, h->csr_kind, h->csr_rest,
+                                  h->forces_raw, h->st);
+            CK(cudaGetLastError());
+            return download_planes<int32_t>(h, h->forces_raw, (int32_t *)dst, 3);
+        }
+        case CS_BUF_ACCUMULATOR:
+            return download_planes<int32_t>(h, h->acc, (int32_t *)dst, 3);
+        case CS_BUF_COUNTS:
+            return download_planes<int32_t>(h, h->count, (int32_t *)dst, 1);
+        default:
+            return fail(CS_E_INVALID, "unknown buffer id");
+    }
+}
+
+extern "C" int cs_write(cs_engine *h, int32_t id, const void *src) {
+    if (!h) return fail(CS_E_INVALID, "null engine");
+    const int64_t P = h->plane;
+    switch (id) {
+        case CS_BUF_POSITIONS:
+        case CS_BUF_VELOCITIES: {
+            if (!src) return fail(CS_E_INVALID, "null source");
+            const int64_t o = id == CS_BUF_VELOCITIES ? 3 * P : 0;
+            if (h->fp64) {
+                float *tmp;
+                CK(cudaMalloc(&tmp, 3 * P * 4));
+                CK(cudaMemsetAsync(tmp, 0, 3 * P * 4, h->st));
+                int r = upload_planes<float>(h, (const float *)src, tmp, 3);
+                if (!r) k_f32_to_f64<<<nb(3 * P), 256, 0, h->st>>>(3 * P, tmp, (double *)h->state[h->cur] + o);
+                CK(cudaStreamSynchronize(h->st));
+                cudaFree(tmp);
+                return r;
+            }
+            int r = upload_planes<float>(h, (const float *)src, (float *)h->state[h->cur] + o, 3);
+            if (!r) CK(cudaStreamSynchronize(h->st));
+            return r;
+        }
+        case CS_BUF_POSITIONS64:
+        case CS_BUF_VELOCITIES64: {
+            if (!h->fp64) return fail(CS_E_INVALID, "float64 buffers need a CS_FLAG_FP64 engine");
+            const int64_t o = id == CS_BUF_VELOCITIES64 ? 3 * P : 0;
+            int r = upload_planes<double>(h, (const double *)src, (double *)h->state[h->cur] + o, 3);
+            if (!r) CK(cudaStreamSynchronize(h->st));
+            return r;
+        }
+        case CS_BUF_EXT_ACCEL: {
+            if (!src) {  // set_external_accel(None): zeros (engine.py:299-300)
+                if (h->has_ext) {
+                    CK(cudaMemsetAsync(h->ext, 0, 3 * P * h->esz, h->st));
+                    CK(cudaStreamSynchronize(h->st));
+                }
+                return 0;
+            }
+            if (!h->ext) {
+                CK(cudaMalloc(&h->ext, 3 * P * h->esz));
+                CK(cudaMemsetAsync(h->ext, 0, 3 * P * h->esz, h->st));
+                drop_graphs(h);  // kernels now read the ext planes
+            }
+            h->has_ext = true;
+            int r;
+            if (h->fp64) {
+                float *tmp;
+                CK(cudaMalloc(&tmp, 3 * P * 4));
+                CK(cudaMemsetAsync(tmp, 0, 3 * P * 4, h->st));
+                r = upload_planes<float>(h, (const float *)src, tmp, 3);
+                if (!r) k_f32_to_f64<<<nb(3 * P), 256, 0, h->st>>>(3 * P, tmp, (double *)h->ext);
+                CK(cudaStreamSynchronize(h->st));
+                cudaFree(tmp);
+            } else {
+                r = upload_planes<float>(h, (const float *)src, (float *)h->ext, 3);
+                if (!r) CK(cudaStreamSynchronize(h->st));
+            }
+            return r;
+        }
+        case CS_BUF_ACCUMULATOR:
+        case CS_BUF_COUNTS: {
+            if (!src) return fail(CS_E_INVALID, "null source");
+            int r = id == CS_BUF_ACCUMULATOR ? upload_planes<int32_t>(h, (const int32_t *)src, h->acc, 3)
+                                             : upload_planes<int32_t>(h, (const int32_t *)src, h->count, 1);
+            if (r) return r;
+            launch_rebuild_touched(h->cargs(), h->rows, h->grid ? h->nx : h->N, h->pitch, h->st);
+            CK(cudaGetLastError());
+            CK(cudaStreamSynchronize(h->st));
+            return 0;
+        }
+        default:
+            return fail(CS_E_INVALID, "unknown or read-only buffer id");
+    }
+}
+
+extern "C" int cs_inject_response(cs_engine *h, int64_t node, const int32_t raw[3], int32_t count) {
+    if (!h) return fail(CS_E_INVALID, "null engine");
+    if (node < 0 || node >= h->N) return fail(CS_E_INVALID, "node index out of range");
+    const int64_t g = h->gidx(node);
+    for (int c = 0; c < 3; ++c)
+        CK(cudaMemcpyAsync(h->acc + c * h->plane + g, raw + c, 4, cudaMemcpyHostToDevice, h->st));
+    CK(cudaMemcpyAsync(h->count + g, &count, 4, cudaMemcpyHostToDevice, h->st));
+    launch_rebuild_touched(h->cargs(), h->rows, h->grid ? h->nx : h->N, h->pitch, h->st);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->st));
+    return 0;
+}
+
+extern "C" int cs_state_plane(cs_engine *h, int32_t which, void **ptr, int64_t *pitch) {
+    if (!h || !ptr || which < 0 || which > 5) return fail(CS_E_INVALID, "bad argument");
+    *ptr = (char *)h->state[h->cur] + (size_t)which * h->plane * h->esz;
+    if (pitch) *pitch = h->pitch;
+    return 0;
+}
+
+extern "C" int cs_kernels_per_frame(cs_engine *h, int32_t *count) {
+    if (!h || !count) return fail(CS_E_INVALID, "null argument");
+    *count = h->kernels_per_frame();
+    return 0;
+}
+
+extern "C" int cs_broadphase_stats(cs_engine *h, int64_t out[4]) {
+    if (!h || !out) return fail(CS_E_INVALID, "null argument");
+    out[0] = h->bp.num_cells;
+    out[1] = h->bp.num_refs;
+    out[2] = h->bp.grid.dims[0];
+    out[3] = h->bp.grid.dims[1] * (int64_t)h->bp.grid.dims[2];
+    return 0;
+}
+
+extern "C" int cs_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+extern "C" int cs_mem_info(int64_t *free_bytes, int64_t *total_bytes) {
+    size_t f = 0, t = 0;
+    CK(cudaMemGetInfo(&f, &t));
+    if (free_bytes) *free_bytes = (int64_t)f;
+    if (total_bytes) *total_bytes = (int64_t)t;
+    return 0;
+}

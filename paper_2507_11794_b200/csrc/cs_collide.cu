@@ -1,0 +1,637 @@
+// cs_collide.cu -- cloth vs static triangle mesh: uniform-grid broad phase
+// (built on device once per obstacle), the two narrow-phase passes and the
+// respond pass.
+//
+// Reference semantics (all bit-exact):
+//   narrow-phase predicate  gpu/kernels.py:136-168 (_segment_triangle_f32),
+//                           collision.py:96-146
+//   pass A (cloth edges)    gpu/kernels.py:186-237, detect_cloth_edges.wgsl
+//   pass B (obstacle edges) gpu/kernels.py:240-290, detect_obstacle_edges.wgsl
+//   accumulation            gpu/kernels.py:171-183 (i32 fixed point, atomics)
+//   respond                 gpu/kernels.py:293-311, respond.wgsl
+//   box prefilter           gpu/kernels.py:55-78 (BOX_PAD = 1e-5)
+//
+// The reference tests every (edge, triangle) pair and rejects most with a
+// padded axis-aligned box test before the Moller-Trumbore algebra.  Here the
+// candidate pairs come from a static uniform grid over the obstacle
+// triangles; each candidate then runs the reference's exact box test and
+// predicate, so the hit set equals the reference's (its own tests assert that
+// prefilter == brute force, test_gpu_engine.py:267-307).  A pair seen from
+// several cells is processed only in the cell holding the minimum corner of
+// the two boxes' intersection, so every pair is tested exactly once.
+//
+// Broad-phase build (construction time; the obstacle is static):
+//   1. per triangle: count covered cells            (k_tri_cell_count)
+//   2. block-wide warp-shuffle exclusive scan        (scan_exclusive)
+//   3. emit (cell key, triangle id) pairs            (k_tri_cell_emit)
+//   4. LSD radix sort of the keys, 8 bits per pass   (radix_sort_pairs)
+//   5. cell [begin, end) by adjacent difference      (k_cell_ranges)
+#include "cs_collide.cuh"
+
+namespace cs {
+
+// ============================================================================
+// scans and radix sort
+// ============================================================================
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+// Exclusive scan of a u32 array in one kernel with chained per-block
+// reductions (three phases: block sums, scan of block sums, block scan).
+constexpr int SCAN_BLOCK = 1024;
+constexpr int SCAN_ITEMS = 4;  // per thread
+constexpr int SCAN_TILE = SCAN_BLOCK * SCAN_ITEMS;
+
+__device__ uint32_t block_excl_scan(uint32_t v, uint32_t *total) {
+    __shared__ uint32_t warp_sums[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t inc = warp_incl_scan(v);
+    if (lane == 31) warp_sums[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+        uint32_t w = lane < nw ? warp_sums[lane] : 0u;
+        w = warp_incl_scan(w);
+        if (lane < nw) warp_sums[lane] = w;
+    }
+    __syncthreads();
+    const uint32_t base = wid ? warp_sums[wid - 1] : 0u;
+    if (total) *total = warp_sums[(blockDim.x >> 5) - 1];
+    __syncthreads();
+    return base + inc - v;
+}
+
+__global__ void k_scan_tiles(const uint32_t *in, uint32_t *out, int64_t n, uint32_t *tile_sums) {
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+    uint32_t v[SCAN_ITEMS], s = 0;
+#pragma unroll
+    for (int q = 0; q < SCAN_ITEMS; ++q) {
+        v[q] = (base + q < n) ? in[base + q] : 0u;
+        s += v[q];
+    }
+    uint32_t total;
+    uint32_t pre = block_excl_scan(s, &total);
+#pragma unroll
+    for (int q = 0; q < SCAN_ITEMS; ++q) {
+        if (base + q < n) out[base + q] = pre;
+        pre += v[q];
+    }
+    if (threadIdx.x == 0 && tile_sums) tile_sums[blockIdx.x] = total;
+}
+
+__global__ void k_add_tile_offsets(uint32_t *out, int64_t n, const uint32_t *tile_offsets) {
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+    const uint32_t add = tile_offsets[blockIdx.x];
+    for (int64_t q = threadIdx.x; q < SCAN_TILE; q += blockDim.x)
+        if (base + q < n) out[base + q] += add;
+}
+
+// out[i] = sum(in[0..i)), recursive over tiles; returns the total via *d_total
+// (device scalar) when given.
+void scan_exclusive(const uint32_t *in, uint32_t *out, int64_t n, DeviceScratch &scratch,
+                    cudaStream_t st) {
+    if (n <= 0) return;
+    const int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    if (tiles == 1) {
+        k_scan_tiles<<<1, SCAN_BLOCK, 0, st>>>(in, out, n, nullptr);
+        return;
+    }
+    uint32_t *sums = (uint32_t *)scratch.get(tiles * sizeof(uint32_t) * 2 + 256);
+    uint32_t *offs = sums + tiles;
+    k_scan_tiles<<<(unsigned)tiles, SCAN_BLOCK, 0, st>>>(in, out, n, sums);
+    DeviceScratch inner;
+    scan_exclusive(sums, offs, tiles, inner, st);
+    k_add_tile_offsets<<<(unsigned)tiles, SCAN_BLOCK, 0, st>>>(out, n, offs);
+    cudaStreamSynchronize(st);  // `inner` is released on return
+}
+
+// ---- LSD radix sort of (key, value) u32 pairs, 8-bit digits -----------------------
+constexpr int RS_BLOCK = 256;
+constexpr int RS_CHUNK = 4096;  // items per block
+
+__global__ void k_radix_hist(const uint32_t *keys, int64_t n, int shift, uint32_t *hist,
+                             int nblocks) {
+    __shared__ uint32_t h[256];
+    for (int d = threadIdx.x; d < 256; d += blockDim.x) h[d] = 0;
+    __syncthreads();
+    const int64_t lo = (int64_t)blockIdx.x * RS_CHUNK;
+    const int64_t hi = min(lo + RS_CHUNK, n);
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x)
+        atomicAdd(&h[(keys[i] >> shift) & 255u], 1u);
+    __syncthreads();
+    // digit-major so one exclusive scan yields every (digit, block) offset
+    for (int d = threadIdx.x; d < 256; d += blockDim.x) hist[(int64_t)d * nblocks + blockIdx.x] = h[d];
+}
+
+// Stable scatter: items of a chunk are ranked in order, 256 at a time; lanes
+// with equal digits are ranked with __match_any_sync.
+__global__ void k_radix_scatter(const uint32_t *keys, const uint32_t *vals, uint32_t *okeys,
+                                uint32_t *ovals, int64_t n, int shift, const uint32_t *offsets,
+                                int nblocks) {
+    __shared__ uint32_t base[256];
+    __shared__ uint32_t wcount[RS_BLOCK / 32][256];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int d = threadIdx.x; d < 256; d += blockDim.x) base[d] = offsets[(int64_t)d * nblocks + blockIdx.x];
+    const int64_t lo = (int64_t)blockIdx.x * RS_CHUNK;
+    const int64_t hi = min(lo + RS_CHUNK, n);
+    for (int64_t t0 = lo; t0 < hi; t0 += RS_BLOCK) {
+        for (int q = threadIdx.x; q < (RS_BLOCK / 32) * 256; q += blockDim.x) (&wcount[0][0])[q] = 0;
+        __syncthreads();
+        const int64_t i = t0 + threadIdx.x;
+        const bool valid = i < hi;
+        const uint32_t k = valid ? keys[i] : 0u;
+        const uint32_t d = valid ? ((k >> shift) & 255u) : 256u;  // 256 never matches a real digit
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+        if (valid && rank == 0) wcount[wid][d] = __popc(peers);
+        __syncthreads();
+        // exclusive prefix over warps for this thread's digit
+        uint32_t before = 0;
+        if (valid)
+            for (int w = 0; w < wid; ++w) before += wcount[w][d];
+        if (valid) {
+            const uint32_t pos = base[d] + before + rank;
+            okeys[pos] = k;
+            ovals[pos] = vals[i];
+        }
+        __syncthreads();
+        // advance per-digit bases by this sub-tile's counts
+        for (int dd = threadIdx.x; dd < 256; dd += blockDim.x) {
+            uint32_t c = 0;
+            for (int w = 0; w < RS_BLOCK / 32; ++w) c += wcount[w][dd];
+            base[dd] += c;
+        }
+        __syncthreads();
+    }
+}
+
+void radix_sort_pairs(uint32_t *keys, uint32_t *vals, uint32_t *tmp_keys, uint32_t *tmp_vals,
+                      int64_t n, int key_bits, DeviceScratch &scratch, cudaStream_t st) {
+    if (n <= 1) return;
+    const int nblocks = (int)((n + RS_CHUNK - 1) / RS_CHUNK);
+    uint32_t *hist = (uint32_t *)scratch.get((size_t)256 * nblocks * sizeof(uint32_t) * 2 + 256);
+    uint32_t *offs = hist + (size_t)256 * nblocks;
+    uint32_t *ka = keys, *va = vals, *kb = tmp_keys, *vb = tmp_vals;
+    int passes = (key_bits + 7) / 8;
+    if (passes < 1) passes = 1;
+    for (int pass = 0; pass < passes; ++pass) {
+        const int shift = pass * 8;
+        k_radix_hist<<<nblocks, RS_BLOCK, 0, st>>>(ka, n, shift, hist, nblocks);
+        DeviceScratch s2;
+        scan_exclusive(hist, offs, (int64_t)256 * nblocks, s2, st);
+        k_radix_scatter<<<nblocks, RS_BLOCK, 0, st>>>(ka, va, kb, vb, n, shift, offs, nblocks);
+        cudaStreamSynchronize(st);
+        uint32_t *t = ka; ka = kb; kb = t;
+        t = va; va = vb; vb = t;
+    }
+    if (ka != keys) {
+        cudaMemcpyAsync(keys, ka, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(vals, va, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
+    }
+}
+
+// ============================================================================
+// broad-phase build
+// ============================================================================
+__device__ __forceinline__ void tri_box(const float *c, float *lo, float *hi) {
+    // kernels.py:62-66 triangle_boxes (unpadded)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        lo[d] = fminf(fminf(c[d], c[3 + d]), c[6 + d]);
+        hi[d] = fmaxf(fmaxf(c[d], c[3 + d]), c[6 + d]);
+    }
+}
+
+__global__ void k_tri_cell_count(const GridDesc g, int64_t nt, const float *__restrict__ corners,
+                                 uint32_t *__restrict__ counts) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    float lo[3], hi[3];
+    tri_box(corners + 9 * t, lo, hi);
+    int a[3], b[3];
+    g.cell_range(lo, hi, a, b);
+    counts[t] = (uint32_t)((b[0] - a[0] + 1) * (b[1] - a[1] + 1) * (b[2] - a[2] + 1));
+}
+
+__global__ void k_tri_cell_emit(const GridDesc g, int64_t nt, const float *__restrict__ corners,
+                                const uint32_t *__restrict__ offsets, uint32_t *__restrict__ keys,
+                                uint32_t *__restrict__ vals) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    float lo[3], hi[3];
+    tri_box(corners + 9 * t, lo, hi);
+    int a[3], b[3];
+    g.cell_range(lo, hi, a, b);
+    uint32_t o = offsets[t];
+    for (int z = a[2]; z <= b[2]; ++z)
+        for (int y = a[1]; y <= b[1]; ++y)
+            for (int x = a[0]; x <= b[0]; ++x) {
+                keys[o] = g.key(x, y, z);
+                vals[o] = (uint32_t)t;
+                ++o;
+            }
+}
+
+__global__ void k_cell_ranges(const uint32_t *__restrict__ keys, int64_t n,
+                              uint32_t *__restrict__ cell_begin, uint32_t *__restrict__ cell_end) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t k = keys[i];
+    if (i == 0 || keys[i - 1] != k) cell_begin[k] = (uint32_t)i;
+    if (i == n - 1 || keys[i + 1] != k) cell_end[k] = (uint32_t)(i + 1);
+}
+
+static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+int build_broadphase(BroadPhase &bp, const float *d_corners, int64_t nt, const float *h_corners,
+                     float cell_size, cudaStream_t st) {
+    // grid over the obstacle's bounding box (host: static data, computed once)
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    double mean_ext = 0.0;
+    for (int64_t t = 0; t < nt; ++t) {
+        float a[3], b[3];
+        for (int d = 0; d < 3; ++d) {
+            const float *c = h_corners + 9 * t;
+            a[d] = fminf(fminf(c[d], c[3 + d]), c[6 + d]);
+            b[d] = fmaxf(fmaxf(c[d], c[3 + d]), c[6 + d]);
+            lo[d] = fminf(lo[d], a[d]);
+            hi[d] = fmaxf(hi[d], b[d]);
+        }
+        mean_ext += fmax(fmax(b[0] - a[0], b[1] - a[1]), b[2] - a[2]);
+    }
+    mean_ext /= (double)(nt > 0 ? nt : 1);
+    float cs_ = cell_size > 0.f ? cell_size : (float)(2.0 * mean_ext);
+    if (!(cs_ > 0.f)) cs_ = 1.0f;
+    int dims[3];
+    for (;;) {
+        int64_t total = 1;
+        for (int d = 0; d < 3; ++d) {
+            dims[d] = (int)ceil((double)(hi[d] - lo[d]) / cs_) + 1;
+            if (dims[d] < 1) dims[d] = 1;
+            total *= dims[d];
+        }
+        if (total <= (int64_t)1 << 24) break;  // keys stay within 24 bits
+        cs_ *= 1.25f;
+    }
+    GridDesc &g = bp.grid;
+    for (int d = 0; d < 3; ++d) {
+        g.origin[d] = lo[d];
+        g.dims[d] = dims[d];
+        g.lo[d] = lo[d];
+        g.hi[d] = hi[d];
+    }
+    g.inv_cell = 1.0f / cs_;
+    g.cell = cs_;
+    bp.num_cells = (int64_t)dims[0] * dims[1] * dims[2];
+
+    uint32_t *counts, *offsets;
+    cudaMalloc(&counts, (nt + 1) * sizeof(uint32_t));
+    cudaMalloc(&offsets, (nt + 1) * sizeof(uint32_t));
+    cudaMemsetAsync(counts, 0, (nt + 1) * sizeof(uint32_t), st);
+    k_tri_cell_count<<<nblk(nt, 256), 256, 0, st>>>(g, nt, d_corners, counts);
+    DeviceScratch scratch;
+    scan_exclusive(counts, offsets, nt + 1, scratch, st);
+    uint32_t total = 0;
+    cudaMemcpyAsync(&total, offsets + nt, sizeof(uint32_t), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    bp.num_refs = total;
+    uint32_t *keys, *vals, *tk, *tv;
+    cudaMalloc(&keys, (total + 1) * sizeof(uint32_t));
+    cudaMalloc(&vals, (total + 1) * sizeof(uint32_t));
+    cudaMalloc(&tk, (total + 1) * sizeof(uint32_t));
+    cudaMalloc(&tv, (total + 1) * sizeof(uint32_t));
+    k_tri_cell_emit<<<nblk(nt, 256), 256, 0, st>>>(g, nt, d_corners, offsets, keys, vals);
+    int bits = 1;
+    while (((int64_t)1 << bits) < bp.num_cells) ++bits;
+    radix_sort_pairs(keys, vals, tk, tv, total, bits, scratch, st);
+    cudaMalloc(&bp.cell_begin, bp.num_cells * sizeof(uint32_t));
+    cudaMalloc(&bp.cell_end, bp.num_cells * sizeof(uint32_t));
+    cudaMemsetAsync(bp.cell_begin, 0, bp.num_cells * sizeof(uint32_t), st);
+    cudaMemsetAsync(bp.cell_end, 0, bp.num_cells * sizeof(uint32_t), st);
+    k_cell_ranges<<<nblk(total, 256), 256, 0, st>>>(keys, total, bp.cell_begin, bp.cell_end);
+    bp.cell_keys = keys;  // sorted keys (kept for the bit-exact assignment test)
+    bp.cell_tris = vals;
+    cudaStreamSynchronize(st);
+    cudaFree(counts);
+    cudaFree(offsets);
+    cudaFree(tk);
+    cudaFree(tv);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+void free_broadphase(BroadPhase &bp) {
+    cudaFree(bp.cell_begin);
+    cudaFree(bp.cell_end);
+    cudaFree(bp.cell_keys);
+    cudaFree(bp.cell_tris);
+    bp = BroadPhase();
+}
+
+// ============================================================================
+// narrow phase
+// ============================================================================
+
+// _segment_triangle_f32 (kernels.py:136-168) with numpy's exact operation order
+__device__ __forceinline__ bool seg_tri(const float *st, const float *en, const float *v0,
+                                        const float *v1, const float *v2, float eps, float *pt) {
+    const float d0 = fsub(en[0], st[0]), d1 = fsub(en[1], st[1]), d2 = fsub(en[2], st[2]);
+    const float d_len = fsqrt(dot3x(d0, d1, d2, d0, d1, d2));
+    if (!(d_len > eps)) return false;
+    const float r0 = fdiv(d0, d_len), r1 = fdiv(d1, d_len), r2 = fdiv(d2, d_len);
+    const float e10 = fsub(v1[0], v0[0]), e11 = fsub(v1[1], v0[1]), e12 = fsub(v1[2], v0[2]);
+    const float e20 = fsub(v2[0], v0[0]), e21 = fsub(v2[1], v0[1]), e22 = fsub(v2[2], v0[2]);
+    const float h0 = fsub(fmul(r1, e22), fmul(r2, e21));
+    const float h1 = fsub(fmul(r2, e20), fmul(r0, e22));
+    const float h2 = fsub(fmul(r0, e21), fmul(r1, e20));
+    const float a = dot3x(e10, e11, e12, h0, h1, h2);
+    if (!(fabsf(a) >= eps)) return false;
+    const float f = fdiv(1.0f, a);
+    const float s0 = fsub(st[0], v0[0]), s1 = fsub(st[1], v0[1]), s2 = fsub(st[2], v0[2]);
+    const float u = fmul(f, dot3x(s0, s1, s2, h0, h1, h2));
+    if (!((u >= 0.f) & (u <= 1.f))) return false;
+    const float q0 = fsub(fmul(s1, e12), fmul(s2, e11));
+    const float q1 = fsub(fmul(s2, e10), fmul(s0, e12));
+    const float q2 = fsub(fmul(s0, e11), fmul(s1, e10));
+    const float v = fmul(f, dot3x(r0, r1, r2, q0, q1, q2));
+    if (!((v >= 0.f) & (fadd(u, v) <= 1.f))) return false;
+    const float t = fmul(f, dot3x(e20, e21, e22, q0, q1, q2));
+    if (!((t > eps) & (t < d_len))) return false;
+    pt[0] = fadd(st[0], fmul(t, r0));
+    pt[1] = fadd(st[1], fmul(t, r1));
+    pt[2] = fadd(st[2], fmul(t, r2));
+    return true;
+}
+
+// np.maximum (NaN propagating)
+__device__ __forceinline__ float np_max(float a, float b) {
+    if (a != a || b != b) return __int_as_float(0x7fc00000);
+    return a >= b ? a : b;
+}
+
+// _accumulate_hits (kernels.py:171-183) for one node; returns true when the
+// node's count went 0 -> 1 (it joins the touched list).
+__device__ __forceinline__ void accumulate(const CollideArgs &A, int64_t g, const float *p,
+                                           const float *hit, const float *on) {
+    const float depth0 = -dot3x(fsub(p[0], hit[0]), fsub(p[1], hit[1]), fsub(p[2], hit[2]), on[0],
+                                on[1], on[2]);
+    const float depth = np_max(depth0, 0.f);
+    const float sc = fadd(depth, A.margin);
+    atomicAdd(A.acc + g, encode_fixed(fmul(on[0], sc), A.scale_f));
+    atomicAdd(A.acc + A.plane + g, encode_fixed(fmul(on[1], sc), A.scale_f));
+    atomicAdd(A.acc + 2 * A.plane + g, encode_fixed(fmul(on[2], sc), A.scale_f));
+    const int old = atomicAdd(A.count + g, 1);
+    if (old == 0) {
+        const uint32_t slot = atomicAdd(A.touched_n, 1u);
+        A.touched[slot] = (uint32_t)g;
+    }
+}
+
+__device__ __forceinline__ void load_pos(const CollideArgs &A, int64_t g, float *p) {
+    p[0] = A.pos[g];
+    p[1] = A.pos[A.plane + g];
+    p[2] = A.pos[2 * A.plane + g];
+}
+
+__device__ __forceinline__ bool box_overlap(const float *la, const float *ha, const float *lb,
+                                            const float *hb) {
+    return (la[0] <= hb[0]) & (lb[0] <= ha[0]) & (la[1] <= hb[1]) & (lb[1] <= ha[1]) &
+           (la[2] <= hb[2]) & (lb[2] <= ha[2]);
+}
+
+// warp-aggregated counter increment; every lane of the warp calls it (the
+// callers have no early returns), so one atomic per warp suffices
+__device__ __forceinline__ void count_hits(unsigned long long *ctr, uint32_t n) {
+    const uint32_t v = __reduce_add_sync(0xffffffffu, n);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(ctr, (unsigned long long)v);
+}
+
+// Pass A: one thread per unique cloth edge, candidates from the grid.
+__global__ void __launch_bounds__(256)
+k_detect_cloth_edges(const CollideArgs A, const GridDesc g, const uint32_t *__restrict__ cbeg,
+                     const uint32_t *__restrict__ cend, const uint32_t *__restrict__ ctri,
+                     const float *__restrict__ corners, const float *__restrict__ normals,
+                     const int32_t *__restrict__ edges, int64_t ne) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    uint32_t hits = 0;
+    if (e < ne) {
+        const int64_t ga = edges[2 * e], gb = edges[2 * e + 1];
+        float st[3], en[3], lo[3], hi[3];
+        load_pos(A, ga, st);
+        load_pos(A, gb, en);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {  // kernels.py:55-59 segment_boxes
+            lo[d] = fsub(fminf(st[d], en[d]), A.pad);
+            hi[d] = fadd(fmaxf(st[d], en[d]), A.pad);
+        }
+        if (g.overlaps(lo, hi)) {
+            int a[3], b[3];
+            g.cell_range(lo, hi, a, b);
+            for (int z = a[2]; z <= b[2]; ++z)
+                for (int y = a[1]; y <= b[1]; ++y)
+                    for (int x = a[0]; x <= b[0]; ++x) {
+                        const uint32_t key = g.key(x, y, z);
+                        const uint32_t c1 = cend[key];
+                        for (uint32_t q = cbeg[key]; q < c1; ++q) {
+                            const uint32_t t = ctri[q];
+                            const float *c = corners + 9 * (int64_t)t;
+                            float tlo[3], thi[3];
+                            tri_box(c, tlo, thi);
+                            if (!box_overlap(lo, hi, tlo, thi)) continue;
+                            // dedup: min corner of the intersection lies in this cell
+                            const float m[3] = {fmaxf(lo[0], tlo[0]), fmaxf(lo[1], tlo[1]),
+                                                fmaxf(lo[2], tlo[2])};
+                            if (g.cell_of(m[0], 0) != x || g.cell_of(m[1], 1) != y ||
+                                g.cell_of(m[2], 2) != z)
+                                continue;
+                            float pt[3];
+                            if (!seg_tri(st, en, c, c + 3, c + 6, A.eps, pt)) continue;
+                            ++hits;
+                            const float *nrm = normals + 3 * (int64_t)t;
+                            const float sa = dot3x(fsub(st[0], pt[0]), fsub(st[1], pt[1]),
+                                                   fsub(st[2], pt[2]), nrm[0], nrm[1], nrm[2]);
+                            const float sb = dot3x(fsub(en[0], pt[0]), fsub(en[1], pt[1]),
+                                                   fsub(en[2], pt[2]), nrm[0], nrm[1], nrm[2]);
+                            const float sign = np_max(sa, sb) >= 0.f ? 1.f : -1.f;
+                            const float on[3] = {fmul(nrm[0], sign), fmul(nrm[1], sign),
+                                                 fmul(nrm[2], sign)};
+                            accumulate(A, ga, st, pt, on);
+                            accumulate(A, gb, en, pt, on);
+                        }
+                    }
+        }
+    }
+    count_hits(A.frame_hits, hits);
+}
+
+// Pass B: one thread per cloth triangle; candidates are obstacle triangles
+// whose box meets the cloth box padded by 2*pad (a superset of the
+// reference's padded-edge-box test, which is then applied exactly per edge).
+__global__ void __launch_bounds__(256)
+k_detect_obstacle_edges(const CollideArgs A, const GridDesc g, const uint32_t *__restrict__ cbeg,
+                        const uint32_t *__restrict__ cend, const uint32_t *__restrict__ ctri,
+                        const float *__restrict__ corners, const float *__restrict__ normals,
+                        const int32_t *__restrict__ tris, int64_t nc) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    uint32_t hits = 0;
+    if (c < nc) {
+        const int64_t n0 = tris[3 * c], n1 = tris[3 * c + 1], n2 = tris[3 * c + 2];
+        float v0[3], v1[3], v2[3];
+        load_pos(A, n0, v0);
+        load_pos(A, n1, v1);
+        load_pos(A, n2, v2);
+        float clo[3], chi[3], qlo[3], qhi[3];
+        const float pad2 = 2.0f * A.pad;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            clo[d] = fminf(fminf(v0[d], v1[d]), v2[d]);
+            chi[d] = fmaxf(fmaxf(v0[d], v1[d]), v2[d]);
+            qlo[d] = clo[d] - pad2;
+            qhi[d] = chi[d] + pad2;
+        }
+        if (g.overlaps(qlo, qhi)) {
+            int a[3], b[3];
+            g.cell_range(qlo, qhi, a, b);
+            for (int z = a[2]; z <= b[2]; ++z)
+                for (int y = a[1]; y <= b[1]; ++y)
+                    for (int x = a[0]; x <= b[0]; ++x) {
+                        const uint32_t key = g.key(x, y, z);
+                        const uint32_t c1 = cend[key];
+                        for (uint32_t q = cbeg[key]; q < c1; ++q) {
+                            const uint32_t t = ctri[q];
+                            const float *cr = corners + 9 * (int64_t)t;
+                            float tlo[3], thi[3];
+                            tri_box(cr, tlo, thi);
+                            if (!box_overlap(qlo, qhi, tlo, thi)) continue;
+                            const float m[3] = {fmaxf(qlo[0], tlo[0]), fmaxf(qlo[1], tlo[1]),
+                                                fmaxf(qlo[2], tlo[2])};
+                            if (g.cell_of(m[0], 0) != x || g.cell_of(m[1], 1) != y ||
+                                g.cell_of(m[2], 2) != z)
+                                continue;
+                            const float *nrm = normals + 3 * (int64_t)t;
+                            for (int slot = 0; slot < 3; ++slot) {
+                                const float *st = cr + 3 * slot;
+                                const float *en = cr + 3 * ((slot + 1) % 3);
+                                float elo[3], ehi[3];
+#pragma unroll
+                                for (int d = 0; d < 3; ++d) {
+                                    elo[d] = fsub(fminf(st[d], en[d]), A.pad);
+                                    ehi[d] = fadd(fmaxf(st[d], en[d]), A.pad);
+                                }
+                                if (!box_overlap(elo, ehi, clo, chi)) continue;
+                                float pt[3];
+                                if (!seg_tri(st, en, v0, v1, v2, A.eps, pt)) continue;
+                                ++hits;
+                                const float t0 = dot3x(fsub(v0[0], pt[0]), fsub(v0[1], pt[1]),
+                                                       fsub(v0[2], pt[2]), nrm[0], nrm[1], nrm[2]);
+                                const float t1 = dot3x(fsub(v1[0], pt[0]), fsub(v1[1], pt[1]),
+                                                       fsub(v1[2], pt[2]), nrm[0], nrm[1], nrm[2]);
+                                const float t2 = dot3x(fsub(v2[0], pt[0]), fsub(v2[1], pt[1]),
+                                                       fsub(v2[2], pt[2]), nrm[0], nrm[1], nrm[2]);
+                                const float total = fadd(fadd(t0, t1), t2);
+                                const float sign = total >= 0.f ? 1.f : -1.f;
+                                const float on[3] = {fmul(nrm[0], sign), fmul(nrm[1], sign),
+                                                     fmul(nrm[2], sign)};
+                                accumulate(A, n0, v0, pt, on);
+                                accumulate(A, n1, v1, pt, on);
+                                accumulate(A, n2, v2, pt, on);
+                            }
+                        }
+                    }
+        }
+    }
+    count_hits(A.frame_hits, hits);
+}
+
+// Respond (kernels.py:293-311) over the touched list only: every node with a
+// nonzero count is on the list exactly once.  Flip-and-halve the velocity,
+// add the decoded (optionally averaged) offset, clear the accumulators.
+__global__ void __launch_bounds__(256)
+k_respond(const CollideArgs A, float *__restrict__ pos, const uint32_t *__restrict__ pinbits,
+          const float *__restrict__ inv_mass, int average) {
+    const uint32_t n = *A.touched_n;
+    uint32_t moved = 0;
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+        const int64_t g = A.touched[q];
+        const int cnt = A.count[g];
+        const bool pinned = inv_mass ? !(inv_mass[g] > 0.f) : ((pinbits[g >> 5] >> (g & 31)) & 1u);
+        if (cnt > 0 && !pinned) {
+            ++moved;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                float dv = decode_fixed(A.acc[d * A.plane + g], A.scale_d);
+                if (average) dv = fdiv(dv, (float)cnt);
+                pos[(3 + d) * A.plane + g] = fmul(pos[(3 + d) * A.plane + g], -0.5f);
+                pos[d * A.plane + g] = fadd(pos[d * A.plane + g], dv);
+            }
+        }
+        A.acc[g] = 0;
+        A.acc[A.plane + g] = 0;
+        A.acc[2 * A.plane + g] = 0;
+        A.count[g] = 0;
+    }
+    count_hits(A.frame_responded, moved);
+}
+
+// After the respond pass: clear the touched list; at the end of a frame also
+// fold the frame's hits into the cumulative hitCounter and record
+// (hits, responded) in the per-frame ring that StepResult reads lazily.
+__global__ void k_respond_end(const CollideArgs A, int end_of_frame) {
+    *A.touched_n = 0;
+    if (end_of_frame) {
+        const unsigned long long f = *A.frame_counter;
+        *A.hit_counter += *A.frame_hits;
+        A.ring[2 * (f % A.ring_size)] = *A.frame_hits;
+        A.ring[2 * (f % A.ring_size) + 1] = *A.frame_responded;
+        *A.frame_counter = f + 1;
+    }
+}
+
+// Rebuild the touched list from the count buffer (after host writes).
+__global__ void k_rebuild_touched(const CollideArgs A, int64_t n_rows, int64_t nx, int64_t pitch) {
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= n_rows * nx) return;
+    const int64_t g = (v / nx) * pitch + (v % nx);
+    if (A.count[g] != 0) {
+        const uint32_t slot = atomicAdd(A.touched_n, 1u);
+        A.touched[slot] = (uint32_t)g;
+    }
+}
+
+void launch_detect(const CollideArgs &A, const BroadPhase &bp, const float *corners,
+                   const float *normals, const int32_t *edges, int64_t ne, const int32_t *tris,
+                   int64_t nc, cudaStream_t st) {
+    if (ne > 0)
+        k_detect_cloth_edges<<<nblk(ne, 256), 256, 0, st>>>(A, bp.grid, bp.cell_begin, bp.cell_end,
+                                                             bp.cell_tris, corners, normals, edges, ne);
+    if (nc > 0)
+        k_detect_obstacle_edges<<<nblk(nc, 256), 256, 0, st>>>(A, bp.grid, bp.cell_begin,
+                                                                bp.cell_end, bp.cell_tris, corners,
+                                                                normals, tris, nc);
+}
+
+void launch_respond(const CollideArgs &A, float *state, const uint32_t *pinbits,
+                    const float *inv_mass, int average, int64_t max_nodes, int num_sms,
+                    bool end_of_frame, cudaStream_t st) {
+    int64_t blocks = (max_nodes + 255) / 256;
+    const int64_t cap = (int64_t)num_sms * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    k_respond<<<(unsigned)blocks, 256, 0, st>>>(A, state, pinbits, inv_mass, average);
+    k_respond_end<<<1, 1, 0, st>>>(A, end_of_frame ? 1 : 0);
+}
+
+void launch_rebuild_touched(const CollideArgs &A, int64_t rows, int64_t nx, int64_t pitch,
+                            cudaStream_t st) {
+    cudaMemsetAsync(A.touched_n, 0, sizeof(uint32_t), st);
+    const int64_t n = rows * nx;
+    if (n > 0) k_rebuild_touched<<<nblk(n, 256), 256, 0, st>>>(A, rows, nx, pitch);
+}
+
+}  // namespace cs

@@ -1,0 +1,501 @@
+"""The drop-in boundary: a B200 ``Engine`` with the reference's API.
+
+Mirrors clothsim/gpu/engine.py:108-394 -- constructor signature
+``Engine(mesh, obstacle=None, params=None, device=None, pair_budget=...)``,
+``step(readback=False, debug=False) -> StepResult``, ``run_respond_pass``,
+``inject_response``, ``set_external_accel``, the ``read_*`` readbacks, the
+writable ``buffers.pos`` / ``buffers.vel`` views, ``build_pipeline`` and
+``step_gpu`` -- plus ``get_adapter`` with the ``CLOTHSIM_ADAPTER`` switch
+(gpu/device.py:156-172).  Every frame runs as hand-written sm_100a kernels
+behind the C ABI of include/clothsim_b200.h; this module only marshals
+arguments.  There is no CPU path: without the CUDA library or a device the
+constructor raises ``AdapterUnavailable``.
+
+Arithmetic modes (keyword-only ``precision=``):
+
+* ``"fast"`` (default) -- fp32 node gather with the 12-spring grid stencil;
+  parity with the reference CPU solver within the north star's tolerances.
+* ``"fixed"`` -- the reference engine's arithmetic (per-spring f32 force,
+  i32 fixed point at ``fixed_point_scale``): bit-identical to the reference's
+  ``gpu.engine.Engine`` in every buffer, hit count and contact.
+* ``"fp64"`` -- float64 gather in the reference solver's operation order:
+  bit-identical to ``solver.step`` (no obstacle).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .errors import AdapterUnavailable, CapacityError, CollisionBudgetError
+from .fixedpoint import encode_values
+from .mesh import SimParams, grid_springs, grid_triangles, grid_unique_edges, unique_edges
+
+__all__ = [
+    "ADAPTER_ENV", "CudaDevice", "get_adapter", "Engine", "StepResult", "Layout",
+    "build_pipeline", "step_gpu", "DEFAULT_PAIR_BUDGET", "PRECISIONS",
+]
+
+ADAPTER_ENV = "CLOTHSIM_ADAPTER"
+DEFAULT_PAIR_BUDGET = 20_000_000  # collision.py:40
+PRECISIONS = ("fast", "fixed", "fp64")
+_F32 = np.float32
+
+
+class CudaDevice:
+    """The compute adapter (gpu/device.py SoftwareDevice's counterpart)."""
+
+    name = "cuda"
+
+    def __init__(self):
+        lib = N.load()
+        count = lib.cs_device_count()
+        if count < 1:
+            raise AdapterUnavailable("no CUDA device is visible to the cloth engine")
+        self.device_count = count
+
+    def mem_info(self):
+        free, total = ctypes.c_int64(), ctypes.c_int64()
+        N.check(N.load().cs_mem_info(ctypes.byref(free), ctypes.byref(total)))
+        return free.value, total.value
+
+
+def get_adapter() -> CudaDevice:
+    """Adapter selection honouring CLOTHSIM_ADAPTER (device.py:156-172):
+    "none" simulates a host without an adapter; "cuda" (default), "b200" and
+    the reference's "software" all select the B200 engine."""
+    choice = os.environ.get(ADAPTER_ENV, "cuda").strip().lower()
+    if choice == "none":
+        raise AdapterUnavailable(f"{ADAPTER_ENV}=none: no compute adapter requested")
+    if choice not in ("", "cuda", "b200", "gpu", "software"):
+        raise AdapterUnavailable(f"unknown {ADAPTER_ENV} value {choice!r}")
+    return CudaDevice()
+
+
+@dataclass
+class Layout:
+    """Buffer census (gpu/layout.py GpuBufferLayout's counts) plus the device
+    bytes this engine allocates."""
+
+    num_nodes: int
+    num_springs: int
+    num_cloth_tris: int
+    num_cloth_edges: int
+    num_obstacle_tris: int
+    state_bytes: int = 0
+    total_bytes: int = 0
+
+    def validate(self, free_bytes: int) -> None:
+        if self.total_bytes > free_bytes:
+            raise CapacityError(
+                f"engine needs {self.total_bytes} B of device memory, {free_bytes} B free")
+
+
+class StepResult:
+    """Per-frame result (engine.py:100-105).  ``hits`` and ``responded`` are
+    read from a device-side ring on first access, so ``step()`` never blocks."""
+
+    __slots__ = ("_engine", "_frame", "_hits", "_responded", "positions", "debug")
+
+    def __init__(self, engine=None, frame=-1, positions=None, debug=None, hits=None,
+                 responded=None):
+        self._engine, self._frame = engine, frame
+        self._hits, self._responded = hits, responded
+        self.positions = positions
+        self.debug = {} if debug is None else debug
+
+    def _resolve(self):
+        if self._hits is None:
+            if self._engine is None or not self._engine.has_obstacle:
+                self._hits, self._responded = 0, 0
+            else:
+                self._hits, self._responded = self._engine._frame_hits(self._frame)
+
+    @property
+    def hits(self) -> int:
+        self._resolve()
+        return self._hits
+
+    @property
+    def responded(self) -> int:
+        self._resolve()
+        return self._responded
+
+    def __repr__(self):
+        return f"StepResult(frame={self._frame}, hits={self.hits}, responded={self.responded})"
+
+
+class _StateView:
+    """numpy-like read/write view of one (N,3) device buffer, so reference
+    code such as ``eng.buffers.vel[0] = (0, 0, 2)`` keeps working."""
+
+    def __init__(self, engine, read_id, write_id):
+        self._e, self._r, self._w = engine, read_id, write_id
+
+    def _get(self):
+        return self._e._read(self._r, np.float32, 3)
+
+    def __array__(self, dtype=None, copy=None):
+        a = self._get()
+        return a if dtype is None else a.astype(dtype)
+
+    def __getitem__(self, idx):
+        return self._get()[idx]
+
+    def __setitem__(self, idx, value):
+        if self._w is None:
+            raise TypeError("this buffer is read-only")
+        a = self._get()
+        a[idx] = value
+        self._e._write(self._w, a.astype(np.float32))
+
+    @property
+    def shape(self):
+        return (self._e.num_nodes, 3)
+
+    dtype = np.dtype(np.float32)
+
+    def copy(self):
+        return self._get()
+
+    def __len__(self):
+        return self._e.num_nodes
+
+
+class PipelineBuffers:
+    def __init__(self, engine):
+        self.pos = _StateView(engine, N.BUF_POSITIONS, N.BUF_POSITIONS)
+        self.vel = _StateView(engine, N.BUF_VELOCITIES, N.BUF_VELOCITIES)
+        self.prev = _StateView(engine, N.BUF_PREV_POSITIONS, None)
+        self.normals = _StateView(engine, N.BUF_NORMALS, None)
+
+
+def _grid_stencil_rest(mesh):
+    """(nx, ny, rest6) when `mesh` holds generate_cloth_grid's exact topology
+    and every spring family/direction has a single f32 rest length (SURVEY.md
+    finding 4); None otherwise (generic CSR path)."""
+    nx, ny = getattr(mesh, "nx", None), getattr(mesh, "ny", None)
+    if nx is None or ny is None or nx < 2 or ny < 2:
+        return None
+    springs = np.asarray(mesh.spring_indices)
+    kinds = np.asarray(mesh.spring_kinds)
+    if len(springs) == 0 or len(np.asarray(mesh.positions)) != nx * ny:
+        return None
+    ref_springs, ref_kinds = grid_springs(nx, ny)
+    if springs.shape != ref_springs.shape or not np.array_equal(springs, ref_springs) \
+            or not np.array_equal(kinds, ref_kinds):
+        return None
+    if not np.array_equal(np.asarray(mesh.triangles), grid_triangles(nx, ny)):
+        return None
+    rest32 = np.asarray(mesh.spring_rest_lengths).astype(_F32)
+    off = springs[:, 1].astype(np.int64) - springs[:, 0]
+    rest6 = []
+    for kind, delta in ((0, 1), (0, nx), (1, nx + 1), (1, nx - 1), (2, 2), (2, 2 * nx)):
+        vals = np.unique(rest32[(kinds == kind) & (off == delta)])
+        if len(vals) > 1:
+            return None
+        rest6.append(float(vals[0]) if len(vals) else 0.0)
+    return nx, ny, rest6
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+class Engine:
+    """A built B200 pipeline bound to one cloth/obstacle/params configuration."""
+
+    def __init__(self, mesh, obstacle=None, params=None, device=None,
+                 pair_budget: int = DEFAULT_PAIR_BUDGET, *, precision: str = "fast",
+                 graph: bool = True, stream=None, cell_size: float | None = None,
+                 force_csr: bool = False):
+        if precision not in PRECISIONS:
+            raise ValueError(f"precision must be one of {PRECISIONS}")
+        self.mesh = mesh
+        self.obstacle = obstacle
+        self.params = params if params is not None else SimParams()
+        self.device = device if device is not None else get_adapter()
+        self.pair_budget = pair_budget
+        self.precision = precision
+        self._lib = N.load()
+        self._handle = None
+        p = self.params
+
+        n = int(len(np.asarray(mesh.positions)))
+        tris = np.ascontiguousarray(mesh.triangles, dtype=np.int32)
+        stencil = _grid_stencil_rest(mesh)
+        if stencil is not None:
+            edges = grid_unique_edges(stencil[0], stencil[1])
+        else:
+            edges = unique_edges(tris) if len(tris) else np.zeros((0, 2), np.int32)
+        has_obs = obstacle is not None and len(obstacle.triangles) > 0
+        n_obs = len(obstacle.triangles) if obstacle is not None else 0
+        springs = np.ascontiguousarray(mesh.spring_indices, dtype=np.int32).reshape(-1, 2)
+        esz = 8 if precision == "fp64" else 4
+        pitch_nodes = ((stencil[0] + 31) // 32 * 32) * stencil[1] if stencil else n
+        state_bytes = 2 * 6 * pitch_nodes * esz
+        total = state_bytes + 3 * pitch_nodes * esz + 24 * pitch_nodes + 12 * len(tris) \
+            + 8 * len(edges) + 48 * n_obs
+        if stencil is None:
+            total += 16 * len(springs) * 2 + 8 * n + 12 * len(tris) + 12 * len(tris) * esz
+        self.layout = Layout(n, len(springs), len(tris), len(edges), n_obs, state_bytes, total)
+        free, _ = self.device.mem_info()
+        self.layout.validate(free)
+
+        # collision.py:258-266 / engine.py:137-142: same census, same refusal
+        self.pairs_per_frame = len(edges) * n_obs + 3 * n_obs * len(tris)
+        if self.pairs_per_frame > pair_budget:
+            raise CollisionBudgetError(
+                f"frame needs {self.pairs_per_frame} edge-triangle tests, "
+                f"budget is {pair_budget}; raise the budget or reduce resolution")
+
+        masses = np.asarray(mesh.masses, dtype=np.float64)
+        pinned = np.asarray(mesh.pinned, dtype=bool)
+        inv = np.ascontiguousarray(np.where(pinned, 0.0, 1.0 / masses).astype(_F32))
+        pos32 = np.ascontiguousarray(np.asarray(mesh.positions).astype(_F32))
+        keep = dict(tris=tris, edges=np.ascontiguousarray(edges, dtype=np.int32), inv=inv,
+                    pos32=pos32, springs=springs,
+                    kinds=np.ascontiguousarray(mesh.spring_kinds, dtype=np.int32),
+                    rest32=np.ascontiguousarray(np.asarray(mesh.spring_rest_lengths).astype(_F32)))
+        d = N.CsDesc()
+        d.abi_version = N.ABI_VERSION
+        flags = 0
+        if p.explicit_euler:
+            flags |= N.FLAG_EXPLICIT_EULER
+        if p.average_response:
+            flags |= N.FLAG_AVERAGE_RESPONSE
+        if precision == "fixed":
+            flags |= N.FLAG_FIXED_POINT
+        if precision == "fp64":
+            flags |= N.FLAG_FP64
+            keep["pos64"] = np.ascontiguousarray(mesh.positions, dtype=np.float64)
+            keep["mass64"] = np.ascontiguousarray(masses)
+            keep["pin8"] = np.ascontiguousarray(pinned.astype(np.uint8))
+            keep["rest64"] = np.ascontiguousarray(mesh.spring_rest_lengths, dtype=np.float64)
+            d.positions64 = _p(keep["pos64"])
+            d.masses64 = _p(keep["mass64"])
+            d.pinned = _p(keep["pin8"])
+            d.spring_rest64 = _p(keep["rest64"])
+        if not graph:
+            flags |= N.FLAG_NO_GRAPH
+        if force_csr:
+            flags |= N.FLAG_FORCE_CSR
+        d.flags = flags
+        if stencil is not None:
+            d.nx, d.ny = stencil[0], stencil[1]
+            for q in range(6):
+                d.grid_rest[q] = stencil[2][q]
+        d.num_nodes = n
+        d.num_springs = len(springs)
+        d.springs = _p(keep["springs"])
+        d.spring_kinds = _p(keep["kinds"])
+        d.spring_rest = _p(keep["rest32"])
+        d.num_tris = len(tris)
+        d.tris = _p(tris)
+        d.num_edges = len(edges)
+        d.edges = _p(keep["edges"])
+        d.positions = _p(pos32)
+        d.inv_mass = _p(inv)
+        if has_obs:
+            corners = np.asarray(obstacle.vertices)[np.asarray(obstacle.triangles)]
+            keep["corners"] = np.ascontiguousarray(corners.astype(_F32))
+            keep["onorm"] = np.ascontiguousarray(np.asarray(obstacle.face_normals).astype(_F32))
+            d.num_obstacle_tris = n_obs
+            d.obstacle_corners = _p(keep["corners"])
+            d.obstacle_normals = _p(keep["onorm"])
+        d.dt = p.dt / p.substeps
+        for q in range(3):
+            d.gravity[q] = float(p.gravity[q])
+            d.stiffness[q] = float(p.stiffness[q])
+        d.damping = float(p.damping)
+        d.epsilon_mt = float(p.epsilon_mt)
+        d.response_margin = float(p.response_margin)
+        d.fixed_point_scale = int(p.fixed_point_scale)
+        d.substeps = int(p.substeps)
+        d.cell_size = float(cell_size) if cell_size else 0.0
+        if stream is not None:
+            d.stream = int(getattr(stream, "cuda_stream", stream))
+        h = ctypes.c_void_p()
+        N.check(self._lib.cs_create(ctypes.byref(d), ctypes.byref(h)))
+        self._handle = h
+        self.kparams = d  # the baked parameter block (engine.py:274-285 KernelParams)
+        self.stencil = stencil is not None
+        self.frame_count = 0
+        self.buffers = PipelineBuffers(self)
+        self._has_obstacle = has_obs
+
+    # -- lifetime -----------------------------------------------------------------
+    def close(self):
+        if self._handle is not None and self._handle.value:
+            self._lib.cs_destroy(self._handle)
+        self._handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- properties ---------------------------------------------------------------
+    @property
+    def num_nodes(self) -> int:
+        return self.layout.num_nodes
+
+    @property
+    def has_obstacle(self) -> bool:
+        return self._has_obstacle
+
+    @property
+    def kernels_per_frame(self) -> int:
+        c = ctypes.c_int32()
+        N.check(self._lib.cs_kernels_per_frame(self._handle, ctypes.byref(c)))
+        return c.value
+
+    def broadphase_stats(self) -> dict:
+        a = (ctypes.c_int64 * 4)()
+        N.check(self._lib.cs_broadphase_stats(self._handle, a))
+        return {"cells": a[0], "refs": a[1], "dims_x": a[2], "dims_yz": a[3]}
+
+    # -- runtime ------------------------------------------------------------------
+    def set_external_accel(self, accel=None) -> None:
+        """Constant per-node acceleration (N, 3), or None to clear (engine.py:297-302)."""
+        if accel is None:
+            N.check(self._lib.cs_write(self._handle, N.BUF_EXT_ACCEL, None))
+            return
+        a = np.ascontiguousarray(np.broadcast_to(np.asarray(accel, dtype=_F32),
+                                                 (self.num_nodes, 3)))
+        N.check(self._lib.cs_write(self._handle, N.BUF_EXT_ACCEL, a.ctypes.data))
+
+    def step(self, readback: bool = False, debug: bool = False) -> StepResult:
+        """Advance one frame (engine.py:304-344)."""
+        frame = self.frame_count
+        snaps = {}
+        if debug:
+            L, h = self._lib, self._handle
+            # the gather keeps no force accumulator: "zeroed" forces are the
+            # registers each node starts its sum from
+            snaps["forces_after_zero"] = np.zeros((self.num_nodes, 3), dtype=np.int32)
+            N.check(L.cs_run_pass(h, N.PASS_FORCE_INTEGRATE))
+            if self.has_obstacle:
+                N.check(L.cs_run_pass(h, N.PASS_DETECT))
+                snaps["accumulator_before_respond"] = self.read_accumulator_raw()
+                snaps["counts_before_respond"] = self.read_counts()
+                N.check(L.cs_run_pass(h, N.PASS_RESPOND))
+                snaps["accumulator_after_respond"] = self.read_accumulator_raw()
+                snaps["counts_after_respond"] = self.read_counts()
+            N.check(L.cs_run_pass(h, N.PASS_NORMALS))
+        else:
+            N.check(self._lib.cs_step(self._handle, 1))
+        self.frame_count += 1
+        res = StepResult(self, frame, debug=snaps)
+        if readback:
+            res.positions = self.read_positions()
+        return res
+
+    def step_frames(self, frames: int) -> None:
+        """Advance `frames` frames with one call (graph replays, no sync)."""
+        N.check(self._lib.cs_step(self._handle, int(frames)))
+        self.frame_count += int(frames)
+
+    def run_respond_pass(self) -> int:
+        """Respond kernel alone (engine.py:346-352); returns nodes moved."""
+        r = ctypes.c_int64()
+        N.check(self._lib.cs_respond(self._handle, ctypes.byref(r)))
+        return int(r.value)
+
+    def inject_response(self, node: int, offset, count: int = 1) -> None:
+        """Write one node's accumulator cells (engine.py:354-358)."""
+        enc = encode_values(np.asarray(offset, dtype=_F32), self.params.fixed_point_scale)
+        raw = (ctypes.c_int32 * 3)(*[int(x) for x in enc])
+        N.check(self._lib.cs_inject_response(self._handle, int(node), raw, int(count)))
+
+    def synchronize(self) -> None:
+        N.check(self._lib.cs_synchronize(self._handle))
+
+    def _frame_hits(self, frame):
+        hits, resp = ctypes.c_int64(), ctypes.c_int64()
+        N.check(self._lib.cs_frame_hits(self._handle, int(frame), ctypes.byref(hits),
+                                        ctypes.byref(resp)))
+        return int(hits.value), int(resp.value)
+
+    def stats(self) -> dict:
+        s = N.CsStats()
+        N.check(self._lib.cs_frame_stats(self._handle, ctypes.byref(s)))
+        return {"hits": s.hits, "responded": s.responded, "frames": s.frames,
+                "hit_counter": s.hit_counter}
+
+    # -- transfers ------------------------------------------------------------------
+    def _read(self, buf, dtype, comps, out=None):
+        shape = (self.num_nodes, comps) if comps > 1 else (self.num_nodes,)
+        if out is None:
+            out = np.empty(shape, dtype=dtype)
+        N.check(self._lib.cs_read(self._handle, buf, out.ctypes.data))
+        return out
+
+    def _write(self, buf, arr):
+        N.check(self._lib.cs_write(self._handle, buf, np.ascontiguousarray(arr).ctypes.data))
+
+    def read_positions(self, out=None) -> np.ndarray:
+        return self._read(N.BUF_POSITIONS, _F32, 3, out)
+
+    def read_velocities(self, out=None) -> np.ndarray:
+        return self._read(N.BUF_VELOCITIES, _F32, 3, out)
+
+    def read_normals(self, out=None) -> np.ndarray:
+        return self._read(N.BUF_NORMALS, _F32, 3, out)
+
+    def read_previous_positions(self) -> np.ndarray:
+        return self._read(N.BUF_PREV_POSITIONS, _F32, 3)
+
+    def read_forces_raw(self) -> np.ndarray:
+        """Spring-only i32 fixed-point forces of the last spring pass
+        (engine.py:368-369), recomputed from the pre-step state with the
+        reference engine's exact arithmetic."""
+        return self._read(N.BUF_FORCES_RAW, np.int32, 3)
+
+    def read_accumulator_raw(self) -> np.ndarray:
+        return self._read(N.BUF_ACCUMULATOR, np.int32, 3)
+
+    def read_counts(self) -> np.ndarray:
+        return self._read(N.BUF_COUNTS, np.int32, 1)
+
+    def read_positions64(self) -> np.ndarray:
+        return self._read(N.BUF_POSITIONS64, np.float64, 3)
+
+    def read_velocities64(self) -> np.ndarray:
+        return self._read(N.BUF_VELOCITIES64, np.float64, 3)
+
+    def write_positions(self, arr) -> None:
+        self._write(N.BUF_POSITIONS, np.asarray(arr, dtype=_F32))
+
+    def write_velocities(self, arr) -> None:
+        self._write(N.BUF_VELOCITIES, np.asarray(arr, dtype=_F32))
+
+    def write_state64(self, pos=None, vel=None) -> None:
+        if pos is not None:
+            self._write(N.BUF_POSITIONS64, np.asarray(pos, dtype=np.float64))
+        if vel is not None:
+            self._write(N.BUF_VELOCITIES64, np.asarray(vel, dtype=np.float64))
+
+    def state_plane(self, which: int):
+        """(device pointer, pitch) of plane `which` (x y z vx vy vz) of the
+        current state -- zero-copy access for the row-band halo exchange."""
+        ptr, pitch = ctypes.c_void_p(), ctypes.c_int64()
+        N.check(self._lib.cs_state_plane(self._handle, int(which), ctypes.byref(ptr),
+                                         ctypes.byref(pitch)))
+        return ptr.value, pitch.value
+
+
+def build_pipeline(mesh, obstacle=None, params=None, device=None,
+                   pair_budget: int = DEFAULT_PAIR_BUDGET, **kw) -> Engine:
+    """Validate and build a ready Engine (engine.py:381-389)."""
+    return Engine(mesh, obstacle, params, device, pair_budget, **kw)
+
+
+def step_gpu(engine: Engine, readback: bool = False, debug: bool = False) -> StepResult:
+    """Function-style alias of Engine.step (engine.py:392-394)."""
+    return engine.step(readback=readback, debug=debug)

@@ -1,0 +1,372 @@
+"""Cloth and obstacle geometry for the B200 engine (inputs of the hot path).
+
+Mirrors the reference data model (clothsim/mesh.py) so reference callers can
+switch packages: ``ClothMesh``, ``TriangleMesh``, ``SimParams``,
+``generate_cloth_grid``, ``generate_icosphere``, ``compute_face_normals``,
+``compute_vertex_normals``, ``unique_edges``, ``spring_count_formula``.
+
+The grid builder is vectorised (the reference loops in Python, ~100 s at
+4096^2) but reproduces the reference topology bit for bit: node (i, j) at
+(i*w/(nx-1), 0, j*h/(ny-1)), flat index j*nx+i; springs ordered structural
+(+i, +j per node), shear (two per cell), bend (+2i, +2j per node); triangles
+(v00, v01, v10), (v10, v01, v11) per cell (mesh.py:223-317).  The Engine also
+accepts the reference's own ClothMesh objects (duck typing).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from enum import IntEnum
+
+import numpy as np
+
+__all__ = [
+    "SpringKind",
+    "ClothMesh",
+    "TriangleMesh",
+    "SimParams",
+    "generate_cloth_grid",
+    "generate_icosphere",
+    "generate_uv_sphere",
+    "compute_face_normals",
+    "compute_vertex_normals",
+    "spring_count_formula",
+    "unique_edges",
+    "grid_unique_edges",
+    "grid_springs",
+    "grid_triangles",
+]
+
+
+class SpringKind(IntEnum):
+    STRUCTURAL = 0
+    SHEAR = 1
+    BEND = 2
+
+
+@dataclass
+class ClothMesh:
+    """Regular nx x ny cloth: SoA node arrays, spring table, triangulation
+    (field meaning as mesh.py:75-124)."""
+
+    nx: int
+    ny: int
+    positions: np.ndarray            # (N, 3) float64 construction pose
+    masses: np.ndarray               # (N,) float64
+    pinned: np.ndarray               # (N,) bool
+    spring_indices: np.ndarray       # (S, 2) int32
+    spring_rest_lengths: np.ndarray  # (S,) float64
+    spring_kinds: np.ndarray         # (S,) int32
+    triangles: np.ndarray            # (C, 3) int32
+
+    @property
+    def num_nodes(self) -> int:
+        return self.nx * self.ny
+
+    @property
+    def num_springs(self) -> int:
+        return len(self.spring_indices)
+
+    def node_index(self, i: int, j: int) -> int:
+        if not (0 <= i < self.nx and 0 <= j < self.ny):
+            raise IndexError(f"grid coordinate ({i}, {j}) outside {self.nx}x{self.ny}")
+        return j * self.nx + i
+
+
+@dataclass
+class TriangleMesh:
+    """Static obstacle: vertices, triangles, unit face normals (mesh.py:127-149)."""
+
+    vertices: np.ndarray
+    triangles: np.ndarray
+    face_normals: np.ndarray = field(default=None)
+
+    def __post_init__(self) -> None:
+        self.vertices = np.asarray(self.vertices, dtype=np.float64)
+        self.triangles = np.asarray(self.triangles, dtype=np.int32)
+        if self.triangles.size and self.triangles.max() >= len(self.vertices):
+            raise ValueError("triangle references a vertex that does not exist")
+        if self.face_normals is None:
+            self.face_normals = compute_face_normals(self.vertices, self.triangles)
+
+    @property
+    def num_vertices(self) -> int:
+        return len(self.vertices)
+
+    @property
+    def num_triangles(self) -> int:
+        return len(self.triangles)
+
+
+@dataclass
+class SimParams:
+    """Simulation coefficients (mesh.py:152-204); same defaults and checks."""
+
+    dt: float = 0.016
+    gravity: tuple = (0.0, -9.8, 0.0)
+    stiffness: object = 50.0
+    damping: float = 0.5
+    epsilon_mt: float = 1e-6
+    response_margin: float = 1e-3
+    fixed_point_scale: int = 1 << 16
+    workgroup_size: int = 256
+    substeps: int = 1
+    explicit_euler: bool = False
+    average_response: bool = True
+
+    def __post_init__(self) -> None:
+        if not self.dt > 0.0:
+            raise ValueError("dt must be positive")
+        if np.shape(self.gravity) != (3,):
+            raise ValueError("gravity must be a 3-vector")
+        self.gravity = tuple(float(g) for g in self.gravity)
+        if np.isscalar(self.stiffness):
+            self.stiffness = (float(self.stiffness),) * 3
+        else:
+            self.stiffness = tuple(float(s) for s in self.stiffness)
+        if len(self.stiffness) != 3:
+            raise ValueError("stiffness needs one value or (structural, shear, bend)")
+        if any(s < 0.0 for s in self.stiffness):
+            raise ValueError("stiffness must be non-negative")
+        if self.damping < 0.0:
+            raise ValueError("damping must be non-negative")
+        if self.epsilon_mt <= 0.0:
+            raise ValueError("epsilon_mt must be positive")
+        if self.response_margin < 0.0:
+            raise ValueError("response_margin must be non-negative")
+        if int(self.fixed_point_scale) < 1:
+            raise ValueError("fixed_point_scale must be >= 1")
+        self.fixed_point_scale = int(self.fixed_point_scale)
+        if int(self.workgroup_size) < 1:
+            raise ValueError("workgroup_size must be >= 1")
+        self.workgroup_size = int(self.workgroup_size)
+        if int(self.substeps) < 1:
+            raise ValueError("substeps must be >= 1")
+        self.substeps = int(self.substeps)
+
+    def stiffness_for(self, kind: int) -> float:
+        return self.stiffness[int(kind)]
+
+
+def spring_count_formula(nx: int, ny: int) -> tuple:
+    """(structural, shear, bend) spring counts of an nx x ny grid (mesh.py:207-220)."""
+    if nx < 2 or ny < 2:
+        raise ValueError("grid needs at least 2 nodes per side")
+    return (nx * (ny - 1) + ny * (nx - 1), 2 * (nx - 1) * (ny - 1),
+            nx * max(ny - 2, 0) + ny * max(nx - 2, 0))
+
+
+def _interleave(cands):
+    """Flatten per-item candidate columns [(a, b, valid), ...] in item-major,
+    column-minor order, keeping valid entries only."""
+    a = np.stack([c[0] for c in cands], axis=1).ravel()
+    b = np.stack([c[1] for c in cands], axis=1).ravel()
+    ok = np.stack([c[2] for c in cands], axis=1).ravel()
+    return a[ok], b[ok]
+
+
+def grid_springs(nx: int, ny: int):
+    """(S,2) int32 endpoints and (S,) int32 kinds in the reference order."""
+    j, i = np.divmod(np.arange(nx * ny, dtype=np.int64), nx)
+    n = j * nx + i
+    sa, sb = _interleave([(n, n + 1, i + 1 < nx), (n, n + nx, j + 1 < ny)])
+    cj, ci = np.divmod(np.arange((nx - 1) * (ny - 1), dtype=np.int64), nx - 1)
+    c = cj * nx + ci
+    ones = np.ones_like(c, dtype=bool)
+    ha, hb = _interleave([(c, c + nx + 1, ones), (c + 1, c + nx, ones)])
+    ba, bb = _interleave([(n, n + 2, i + 2 < nx), (n, n + 2 * nx, j + 2 < ny)])
+    pairs = np.stack([np.concatenate([sa, ha, ba]), np.concatenate([sb, hb, bb])], axis=1)
+    kinds = np.concatenate([np.zeros(len(sa), np.int32), np.ones(len(ha), np.int32),
+                            np.full(len(ba), 2, np.int32)])
+    return pairs.astype(np.int32), kinds
+
+
+def grid_triangles(nx: int, ny: int) -> np.ndarray:
+    """(C,3) int32: per cell (v00, v01, v10), (v10, v01, v11) (mesh.py:296-305)."""
+    cj, ci = np.divmod(np.arange((nx - 1) * (ny - 1), dtype=np.int64), nx - 1)
+    v00 = cj * nx + ci
+    v10, v01, v11 = v00 + 1, v00 + nx, v00 + nx + 1
+    t = np.stack([np.stack([v00, v01, v10], 1), np.stack([v10, v01, v11], 1)], axis=1)
+    return t.reshape(-1, 3).astype(np.int32)
+
+
+def grid_unique_edges(nx: int, ny: int) -> np.ndarray:
+    """unique_edges(grid_triangles(nx, ny)) in closed form: node a's edges to
+    larger indices are a+1 (if i < nx-1), a+nx-1 (the cell diagonal v10-v01,
+    if i > 0 and j < ny-1) and a+nx (if j < ny-1), already in sorted order."""
+    j, i = np.divmod(np.arange(nx * ny, dtype=np.int64), nx)
+    n = j * nx + i
+    a, b = _interleave([(n, n + 1, i + 1 < nx), (n, n + nx - 1, (i > 0) & (j + 1 < ny)),
+                        (n, n + nx, j + 1 < ny)])
+    return np.stack([a, b], axis=1).astype(np.int32)
+
+
+def generate_cloth_grid(nx: int, ny: int, width: float = 1.0, height: float = 1.0,
+                        total_mass: float = None, pinned_rows=None) -> ClothMesh:
+    """Regular cloth grid in the xz-plane at y=0 (mesh.py:223-317)."""
+    if nx < 2 or ny < 2:
+        raise ValueError("grid needs at least 2 nodes per side")
+    if width <= 0.0 or height <= 0.0:
+        raise ValueError("cloth dimensions must be positive")
+    n = nx * ny
+    if total_mass is None:
+        total_mass = 0.05 * n
+    if total_mass <= 0.0:
+        raise ValueError("total_mass must be positive")
+    positions = np.zeros((n, 3), dtype=np.float64)
+    positions[:, 0] = np.tile(np.linspace(0.0, width, nx), ny)
+    positions[:, 2] = np.repeat(np.linspace(0.0, height, ny), nx)
+    masses = np.full(n, total_mass / n, dtype=np.float64)
+    pinned = np.zeros(n, dtype=bool)
+    for j in _resolve_pinned_rows(pinned_rows, ny):
+        pinned[j * nx:(j + 1) * nx] = True
+    springs, kinds = grid_springs(nx, ny)
+    delta = positions[springs[:, 1]] - positions[springs[:, 0]]
+    rest = np.linalg.norm(delta, axis=1)
+    return ClothMesh(nx=nx, ny=ny, positions=positions, masses=masses, pinned=pinned,
+                     spring_indices=springs, spring_rest_lengths=rest, spring_kinds=kinds,
+                     triangles=grid_triangles(nx, ny))
+
+
+def _resolve_pinned_rows(pinned_rows, ny: int):
+    if pinned_rows is None or (isinstance(pinned_rows, str) and pinned_rows == "none"):
+        return []
+    if isinstance(pinned_rows, str):
+        if pinned_rows == "first":
+            return [0]
+        if pinned_rows == "last":
+            return [ny - 1]
+        raise ValueError(f"unknown pinned_rows {pinned_rows!r}")
+    rows = [int(j) for j in pinned_rows]
+    for j in rows:
+        if not 0 <= j < ny:
+            raise ValueError(f"pinned row {j} outside grid with ny={ny}")
+    return rows
+
+
+# --------------------------------------------------------------------------------
+# obstacles
+# --------------------------------------------------------------------------------
+_PHI = (1.0 + math.sqrt(5.0)) / 2.0
+# 12 icosahedron vertices (three golden rectangles) and its 20 outward faces,
+# in the reference's order (mesh.py:334-347)
+_ICO_V = np.array([
+    (-1, _PHI, 0), (1, _PHI, 0), (-1, -_PHI, 0), (1, -_PHI, 0),
+    (0, -1, _PHI), (0, 1, _PHI), (0, -1, -_PHI), (0, 1, -_PHI),
+    (_PHI, 0, -1), (_PHI, 0, 1), (-_PHI, 0, -1), (-_PHI, 0, 1)], dtype=np.float64)
+_ICO_F = np.array([
+    (0, 11, 5), (0, 5, 1), (0, 1, 7), (0, 7, 10), (0, 10, 11),
+    (1, 5, 9), (5, 11, 4), (11, 10, 2), (10, 7, 6), (7, 1, 8),
+    (3, 9, 4), (3, 4, 2), (3, 2, 6), (3, 6, 8), (3, 8, 9),
+    (4, 9, 5), (2, 4, 11), (6, 2, 10), (8, 6, 7), (9, 8, 1)], dtype=np.int64)
+
+
+def generate_icosphere(subdivisions: int, radius: float = 1.0, center=(0.0, 0.0, 0.0)) -> TriangleMesh:
+    """Subdivided icosahedron on a sphere (mesh.py:350-387): 20*4^k faces.
+
+    Each level splits a face (a, b, c) into (a, ab, ca), (b, bc, ab),
+    (c, ca, bc), (ab, bc, ca); an edge's midpoint vertex is created the first
+    time a face (in face order) visits the edge, checked in the order ab, bc,
+    ca -- the same numbering the reference produces.
+    """
+    if subdivisions < 0:
+        raise ValueError("subdivisions must be >= 0")
+    if radius <= 0.0:
+        raise ValueError("radius must be positive")
+    verts = [v / np.linalg.norm(v) for v in _ICO_V]
+    faces = _ICO_F.copy()
+    for _ in range(subdivisions):
+        mid = {}
+        out = np.empty((4 * len(faces), 3), dtype=np.int64)
+        for f, (a, b, c) in enumerate(faces.tolist()):
+            ids = []
+            for u, v in ((a, b), (b, c), (c, a)):
+                key = (u, v) if u < v else (v, u)
+                k = mid.get(key)
+                if k is None:
+                    m = verts[u] + verts[v]
+                    m /= np.linalg.norm(m)
+                    verts.append(m)
+                    k = mid[key] = len(verts) - 1
+                ids.append(k)
+            ab, bc, ca = ids
+            out[4 * f:4 * f + 4] = ((a, ab, ca), (b, bc, ab), (c, ca, bc), (ab, bc, ca))
+        faces = out
+    vertices = np.array(verts) * radius + np.asarray(center, dtype=np.float64)
+    return TriangleMesh(vertices=vertices, triangles=faces.astype(np.int32))
+
+
+def generate_uv_sphere(slices: int = 224, stacks: int = 224, radius: float = 0.3,
+                       center=(0.0, 0.0, 0.0)) -> TriangleMesh:
+    """Procedural latitude/longitude sphere, outward (CCW from outside) faces.
+
+    slices x stacks = 224 x 224 gives 49,954 vertices and 99,904 triangles: the
+    paper's Dragon class (50K vertices / 100K triangles), used by
+    BASELINE configs 3 and 4.
+    """
+    if slices < 3 or stacks < 2:
+        raise ValueError("need slices >= 3 and stacks >= 2")
+    theta = np.pi * np.arange(1, stacks) / stacks            # polar angle of the rings
+    phi = 2.0 * np.pi * np.arange(slices) / slices
+    st, ct = np.sin(theta)[:, None], np.cos(theta)[:, None]
+    ring = np.stack([st * np.cos(phi)[None, :], np.broadcast_to(ct, (stacks - 1, slices)),
+                     st * np.sin(phi)[None, :]], axis=-1).reshape(-1, 3)
+    verts = np.concatenate([[[0.0, 1.0, 0.0]], ring, [[0.0, -1.0, 0.0]]]) * radius
+    verts = verts + np.asarray(center, dtype=np.float64)
+    top, bot = 0, 1 + (stacks - 1) * slices
+    s = np.arange(slices)
+    s1 = (s + 1) % slices
+    tris = [np.stack([np.full(slices, top), 1 + s1, 1 + s], 1)]
+    for r in range(stacks - 2):
+        a = 1 + r * slices + s
+        b = 1 + r * slices + s1
+        c = 1 + (r + 1) * slices + s
+        d = 1 + (r + 1) * slices + s1
+        tris.append(np.stack([np.stack([a, b, c], 1), np.stack([b, d, c], 1)], 1).reshape(-1, 3))
+    last = 1 + (stacks - 2) * slices
+    tris.append(np.stack([last + s, last + s1, np.full(slices, bot)], 1))
+    return TriangleMesh(vertices=verts, triangles=np.concatenate(tris).astype(np.int32))
+
+
+def compute_face_normals(vertices: np.ndarray, triangles: np.ndarray) -> np.ndarray:
+    """Unit float64 face normals; zero-area faces get +y (mesh.py:390-401)."""
+    v = np.asarray(vertices, dtype=np.float64)
+    t = np.asarray(triangles)
+    n = np.cross(v[t[:, 1]] - v[t[:, 0]], v[t[:, 2]] - v[t[:, 0]])
+    length = np.linalg.norm(n, axis=1)
+    ok = length > 1e-30
+    out = np.tile(np.array([0.0, 1.0, 0.0]), (len(t), 1))
+    out[ok] = n[ok] / length[ok, None]
+    return out
+
+
+def compute_vertex_normals(mesh, positions: np.ndarray = None) -> np.ndarray:
+    """Host float64 vertex normals (mesh.py:404-434), for inspection only --
+    the engine computes normals on the device every frame."""
+    if positions is None:
+        positions = getattr(mesh, "positions", None)
+        if positions is None:
+            positions = mesh.vertices
+    p = np.asarray(positions, dtype=np.float64)
+    t = np.asarray(mesh.triangles)
+    n = np.cross(p[t[:, 1]] - p[t[:, 0]], p[t[:, 2]] - p[t[:, 0]])
+    length = np.linalg.norm(n, axis=1)
+    ok = length > 1e-30
+    face = np.zeros_like(n)
+    face[ok] = n[ok] / length[ok, None]
+    acc = np.zeros_like(p)
+    for corner in range(3):
+        np.add.at(acc, t[:, corner], face)
+    ln = np.linalg.norm(acc, axis=1)
+    good = ln > 1e-30
+    out = np.tile(np.array([0.0, 1.0, 0.0]), (len(p), 1))
+    out[good] = acc[good] / ln[good, None]
+    return out
+
+
+def unique_edges(triangles: np.ndarray) -> np.ndarray:
+    """Sorted undirected edge set of a triangulation (mesh.py:437-442)."""
+    t = np.asarray(triangles)
+    e = np.sort(np.concatenate([t[:, [0, 1]], t[:, [1, 2]], t[:, [2, 0]]]), axis=1)
+    return np.unique(e, axis=0).astype(np.int32)

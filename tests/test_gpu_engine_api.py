@@ -1,0 +1,198 @@
+"""The reference's engine tests (pkg/tests/test_gpu_engine.py,
+test_acceptance.py), re-run against the B200 Engine through the same API."""
+
+import numpy as np
+import pytest
+
+import paper_2507_11794_b200 as P
+from oracle import oracle as O
+from paper_2507_11794_b200 import SimParams, generate_cloth_grid, generate_icosphere
+
+pytestmark = pytest.mark.gpu
+SCALE = 1 << 16
+
+
+@pytest.mark.parametrize("precision", ["fixed", "fast"])
+def test_spring_forces_match_reference_solver(rng, precision):
+    """test_gpu_engine.py:92-106 (forces within 5e-4 of the f64 solver)."""
+    mesh = generate_cloth_grid(6, 6)
+    mesh.positions += rng.normal(scale=0.02, size=mesh.positions.shape)
+    vel = rng.normal(scale=0.3, size=mesh.positions.shape).astype(np.float32)
+    params = SimParams(gravity=(0.0, 0.0, 0.0), stiffness=30.0, damping=0.4)
+    eng = P.Engine(mesh, params=params, precision=precision)
+    eng.buffers.vel[...] = vel
+    eng.step()
+    gpu = P.decode_values(eng.read_forces_raw(), SCALE, float32=False)
+    so = O.SolverOracle(mesh, params)
+    so.vel[...] = vel.astype(np.float64)
+    np.testing.assert_allclose(gpu, so.forces_now(), atol=5e-4)
+
+
+def test_golden_perturbed_forces_bit_exact():
+    from conftest import load_golden
+
+    k = load_golden("kats.npz")
+    mesh = generate_cloth_grid(6, 6)
+    mesh.positions = k["pert_positions"]
+    params = SimParams(gravity=(0.0, 0.0, 0.0), stiffness=30.0, damping=0.4)
+    eng = P.Engine(mesh, params=params, precision="fixed")
+    eng.buffers.vel[...] = k["pert_vel"]
+    eng.step()
+    np.testing.assert_array_equal(eng.read_forces_raw(), k["pert_eng_forces"])
+    np.testing.assert_array_equal(eng.read_positions(), k["pert_eng_pos1"])
+    np.testing.assert_array_equal(eng.read_velocities(), k["pert_eng_vel1"])
+
+
+@pytest.mark.parametrize("precision", ["fixed", "fast"])
+def test_rest_cloth_force_buffer_is_exactly_zero_integers(precision):
+    eng = P.Engine(generate_cloth_grid(24, 24), params=SimParams(), precision=precision)
+    eng.step()
+    raw = eng.read_forces_raw()
+    assert raw.dtype == np.int32 and not raw.any()
+    calm = P.Engine(generate_cloth_grid(24, 24), params=SimParams(gravity=(0, 0, 0)),
+                    precision=precision)
+    for _ in range(3):
+        calm.step()
+        assert not calm.read_forces_raw().any()
+
+
+@pytest.mark.parametrize("precision", ["fixed", "fast"])
+def test_gravity_lives_in_integrate(precision):
+    eng = P.Engine(generate_cloth_grid(3, 3),
+                   params=SimParams(dt=0.25, gravity=(0.0, -2.0, 0.0), damping=0.0),
+                   precision=precision)
+    eng.step()
+    np.testing.assert_allclose(eng.read_velocities()[:, 1], np.float32(-0.5), atol=1e-7)
+    assert not eng.read_forces_raw().any()
+
+
+@pytest.mark.parametrize("precision", ["fixed", "fast", "fp64"])
+def test_external_accel_buffer_feeds_integrate(precision):
+    eng = P.Engine(generate_cloth_grid(2, 2), params=SimParams(dt=0.5, gravity=(0, 0, 0)),
+                   precision=precision)
+    eng.set_external_accel(np.tile([4.0, 0.0, 0.0], (4, 1)))
+    eng.step()
+    np.testing.assert_allclose(eng.read_velocities()[:, 0], np.float32(2.0))
+    eng.set_external_accel(None)
+    eng.step()
+    np.testing.assert_allclose(eng.read_velocities()[:, 0], np.float32(2.0))
+
+
+@pytest.mark.parametrize("precision", ["fixed", "fast"])
+def test_pinned_rows_are_bit_frozen(precision):
+    mesh = generate_cloth_grid(4, 4, pinned_rows="first")
+    eng = P.Engine(mesh, params=SimParams(stiffness=10.0, damping=0.1), precision=precision)
+    baked = mesh.positions.astype(np.float32)[mesh.pinned]
+    for _ in range(50):
+        eng.step()
+    np.testing.assert_array_equal(eng.read_positions()[mesh.pinned], baked)
+    assert not eng.read_velocities()[mesh.pinned].any()
+    moved = np.abs(eng.read_positions()[~mesh.pinned] - mesh.positions.astype(np.float32)[~mesh.pinned])
+    assert moved.max() > 1e-4
+
+
+def test_hanging_run_tracks_reference_solver():
+    """test_gpu_engine.py:149-158: 8x8 hanging at the reference dt 0.016."""
+    sc = P.build_scene(P.ScenarioConfig("hanging", (8, 8)))
+    for precision in ("fast", "fixed", "fp64"):
+        eng = P.Engine(sc.mesh, params=sc.params, precision=precision)
+        so = O.SolverOracle(sc.mesh, sc.params)
+        for _ in range(20):
+            eng.step()
+            so.step()
+        assert np.abs(eng.read_positions().astype(np.float64) - so.pos).max() <= 1e-3
+
+
+def test_vertex_normals_match_host_recomputation():
+    sc = P.build_scene(P.ScenarioConfig("hanging", (8, 8)))
+    for precision in ("fast", "fixed"):
+        eng = P.Engine(sc.mesh, params=sc.params, precision=precision)
+        for _ in range(10):
+            eng.step()
+        want = P.compute_vertex_normals(sc.mesh, positions=eng.read_positions().astype(np.float64))
+        np.testing.assert_allclose(eng.read_normals(), want, atol=1e-5)
+
+
+@pytest.mark.parametrize("precision", ["fixed", "fast"])
+def test_two_runs_are_bit_identical_including_contact(precision):
+    cfg = P.ScenarioConfig("drop", (10, 10), obstacle="icosphere:1")
+
+    def run():
+        sc = P.build_scene(cfg)
+        eng = P.Engine(sc.mesh, obstacle=sc.obstacle, params=sc.params, precision=precision)
+        hits = sum(eng.step().hits for _ in range(60))
+        return eng.read_positions().tobytes(), eng.read_velocities().tobytes(), hits
+
+    a, b = run(), run()
+    assert a[2] == b[2] and a[2] > 0
+    assert a[0] == b[0] and a[1] == b[1]
+
+
+def test_respond_trace_flips_velocity_and_applies_decoded_offset():
+    mesh = generate_cloth_grid(2, 2)
+    eng = P.Engine(mesh, params=SimParams())
+    eng.buffers.vel[0] = (0.0, 0.0, 2.0)
+    eng.inject_response(0, (0.0, 0.1, 0.0), count=1)
+    assert eng.run_respond_pass() == 1
+    np.testing.assert_array_equal(eng.read_velocities()[0], np.float32((0.0, 0.0, -1.0)))
+    shift = eng.read_positions()[0] - mesh.positions[0].astype(np.float32)
+    assert shift[1] == np.float32(6554 / SCALE)
+    assert not eng.read_accumulator_raw().any()
+    assert not eng.read_counts().any()
+
+
+def test_respond_averages_and_raw_sum_flag():
+    mesh = generate_cloth_grid(2, 2)
+    want_raw = np.float32(int(P.encode_values(np.array([0.2]), SCALE)[0]) / SCALE)
+    eng = P.Engine(mesh, params=SimParams())
+    eng.inject_response(1, (0.2, 0.0, 0.0), count=2)
+    eng.run_respond_pass()
+    assert eng.read_positions()[1, 0] - np.float32(mesh.positions[1, 0]) == want_raw / np.float32(2)
+    eng = P.Engine(mesh, params=SimParams(average_response=False))
+    eng.inject_response(1, (0.2, 0.0, 0.0), count=2)
+    eng.run_respond_pass()
+    assert eng.read_positions()[1, 0] - np.float32(mesh.positions[1, 0]) == want_raw
+
+
+def test_respond_skips_pinned_nodes_but_still_clears():
+    mesh = generate_cloth_grid(2, 2, pinned_rows="first")
+    eng = P.Engine(mesh, params=SimParams())
+    k = int(np.flatnonzero(mesh.pinned)[0])
+    eng.inject_response(k, (0.0, 0.5, 0.0), count=1)
+    assert eng.run_respond_pass() == 0
+    np.testing.assert_array_equal(eng.read_positions()[k], mesh.positions[k].astype(np.float32))
+    assert not eng.read_counts().any() and not eng.read_accumulator_raw().any()
+
+
+def test_dropped_cloth_drapes_without_tunneling():
+    """test_acceptance.py:146-172 (24x24 on icosphere:2, 600 frames)."""
+    sc = P.build_scene(P.ScenarioConfig("drop", (24, 24), obstacle="icosphere:2"))
+    eng = P.Engine(sc.mesh, obstacle=sc.obstacle, params=sc.params)
+    results = [eng.step() for _ in range(600)]
+    total = sum(r.hits for r in results[-4000:])
+    pos = eng.read_positions().astype(np.float64)
+    dist = np.linalg.norm(pos - sc.sphere_center, axis=1)
+    floor = sc.sphere_radius - sc.params.response_margin
+    assert total > 0
+    assert np.mean(dist >= floor - 1e-12) >= 0.99
+
+
+def test_budget_and_aliases():
+    with pytest.raises(P.CollisionBudgetError, match="budget"):
+        P.Engine(generate_cloth_grid(8, 8), obstacle=generate_icosphere(1, radius=0.3),
+                 pair_budget=10)
+    eng = P.build_pipeline(generate_cloth_grid(3, 3), params=SimParams())
+    silent = P.step_gpu(eng)
+    assert isinstance(silent, P.StepResult) and silent.positions is None
+    chatty = P.step_gpu(eng, readback=True)
+    assert chatty.positions.shape == (9, 3)
+    assert eng.num_nodes == 9 and not eng.has_obstacle and eng.frame_count == 2
+
+
+def test_capacity_error_for_impossible_layouts():
+    class Tiny(P.CudaDevice):
+        def mem_info(self):
+            return 4096, 4096
+
+    with pytest.raises(P.CapacityError):
+        P.Engine(generate_cloth_grid(64, 64), device=Tiny())
