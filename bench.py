@@ -179,7 +179,8 @@ def main():
     import torch
 
     torch.cuda.init()
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # a real stream: the legacy default (0) would mean "own stream"
+    torch.cuda.set_stream(stream)
     n = scene.mesh.num_nodes
     eng = P.Engine(scene.mesh, scene.obstacle, scene.params, pair_budget=10**13,
                    precision="fast", stream=stream.cuda_stream)
@@ -282,7 +283,8 @@ def main():
 
 def collision_bench(P, torch, args):
     scene = P.baseline_scene("C3")
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # a real stream: the legacy default (0) would mean "own stream"
+    torch.cuda.set_stream(stream)
     eng = P.Engine(scene.mesh, scene.obstacle, scene.params, pair_budget=10**13,
                    precision="fast", stream=stream.cuda_stream)
     eng.step_frames(200)  # drape onto the sphere before timing

@@ -61,6 +61,9 @@ extern "C" {
                                        replaying a captured CUDA graph */
 #define CS_FLAG_FORCE_CSR 32u       /* use the generic per-node CSR gather even
                                        when the topology is a regular grid */
+#define CS_FLAG_TILE_KERNEL 64u     /* grid path: the shared-memory tile kernel
+                                       (every node evaluates its 12 springs)
+                                       instead of the warp-strip kernel */
 
 typedef struct cs_engine cs_engine;
 

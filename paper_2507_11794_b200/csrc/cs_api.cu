@@ -80,6 +80,8 @@ struct cs_engine {
     int64_t nc = 0, ne = 0, nt = 0;
 
     bool has_obstacle = false;
+    bool strip = true;          // grid path uses the warp-strip kernel (cs_strip.cu)
+    bool normals_stale = false; // normals buffer holds the previous frame's (fused)
     float *corners = nullptr, *onormals = nullptr;
     BroadPhase bp;
     int32_t *acc = nullptr, *count = nullptr;
@@ -121,7 +123,7 @@ struct cs_engine {
     int kernels_per_frame() const {
         int k = substeps;  // one fused force+integrate launch per substep
         if (has_obstacle) k += 2 /*detect*/ + 2 /*respond + frame_end*/;
-        k += grid ? 1 : 2;  // normals
+        if (!(grid && strip)) k += grid ? 1 : 2;  // normals (fused into the strip kernel)
         return k;
     }
 };
@@ -200,13 +202,18 @@ static void drop_graphs(cs_engine *h) {
 // ---------------------------------------------------------------------------
 // passes
 // ---------------------------------------------------------------------------
-static void pass_force_integrate(cs_engine *h) {
+static void pass_force_integrate(cs_engine *h, bool fuse_normals = false) {
     for (int s = 0; s < h->substeps; ++s) {
         const int src = h->cur, dst = 1 - h->cur;
         if (h->fp64) {
             launch_csr_step_f64(h->cp, (const double *)h->state[src], (double *)h->state[dst],
                                 h->csr_off, h->csr_nbr, h->csr_kind, h->csr_rest64, h->mass64,
                                 h->pinned8, h->has_ext ? (const double *)h->ext : nullptr, h->st);
+        } else if (h->grid && h->strip) {
+            // normals of the frame's starting state ride along in the first substep
+            launch_strip_step(h->sp, h->fixed, fuse_normals && s == 0, (const float *)h->state[src],
+                              (float *)h->state[dst], h->pinbits,
+                              h->has_ext ? (const float *)h->ext : nullptr, (float *)h->normals, h->st);
         } else if (h->grid) {
             launch_grid_step(h->sp, h->fixed, (const float *)h->state[src], (float *)h->state[dst],
                              h->pinbits, h->has_ext ? (const float *)h->ext : nullptr, h->st);
@@ -247,13 +254,25 @@ static void pass_normals(cs_engine *h) {
     }
 }
 
+// One frame (engine.py:304-344).  On the strip path the normal_update of
+// frame t runs inside frame t+1's force pass; the buffer is marked stale and
+// refreshed by a stand-alone normals launch only when it is read.
 static void launch_frame(cs_engine *h) {
-    pass_force_integrate(h);
+    const bool fuse = h->grid && h->strip;
+    pass_force_integrate(h, fuse);
     if (h->has_obstacle) {
         pass_detect(h);
         pass_respond(h);
     }
-    pass_normals(h);
+    if (!fuse) pass_normals(h);
+    h->normals_stale = fuse;
+}
+
+static void flush_normals(cs_engine *h) {
+    if (h->normals_stale) {
+        pass_normals(h);
+        h->normals_stale = false;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -287,6 +306,7 @@ static int build(cs_engine *h, const cs_desc *d) {
             else if (v != im_free) { uniform = false; break; }
         }
     }
+    h->strip = !(d->flags & CS_FLAG_TILE_KERNEL);
     h->grid = d->nx >= 2 && d->ny >= 2 && (int64_t)d->nx * d->ny == N && !h->fp64 && uniform &&
               !(d->flags & CS_FLAG_FORCE_CSR);
     h->esz = h->fp64 ? 8 : 4;
@@ -573,6 +593,7 @@ extern "C" int cs_step(cs_engine *h, int32_t frames) {
             // replay the parity bookkeeping of one frame
             if (h->substeps & 1) h->cur = 1 - start;
             h->forces_valid = true;
+            h->normals_stale = h->grid && h->strip;
         } else {
             launch_frame(h);
             CK(cudaGetLastError());
@@ -585,12 +606,12 @@ extern "C" int cs_step(cs_engine *h, int32_t frames) {
 extern "C" int cs_run_pass(cs_engine *h, int32_t pass_id) {
     if (!h) return fail(CS_E_INVALID, "null engine");
     switch (pass_id) {
-        case CS_PASS_FORCE_INTEGRATE: pass_force_integrate(h); break;
+        case CS_PASS_FORCE_INTEGRATE: flush_normals(h); pass_force_integrate(h); break;
         case CS_PASS_DETECT: pass_detect(h); break;
         case CS_PASS_RESPOND:
             if (h->has_obstacle) pass_respond(h);
             break;
-        case CS_PASS_NORMALS: pass_normals(h); h->frames++; break;
+        case CS_PASS_NORMALS: pass_normals(h); h->normals_stale = false; h->frames++; break;
         default: return fail(CS_E_INVALID, "unknown pass id");
     }
     CK(cudaGetLastError());
@@ -599,6 +620,7 @@ extern "C" int cs_run_pass(cs_engine *h, int32_t pass_id) {
 
 extern "C" int cs_respond(cs_engine *h, int64_t *responded) {
     if (!h) return fail(CS_E_INVALID, "null engine");
+    flush_normals(h);  // the buffer must describe the pre-respond positions
     CK(cudaMemsetAsync(h->stats + 1, 0, sizeof(unsigned long long), h->st));
     launch_respond(h->cargs(), (float *)h->state[h->cur], h->grid ? h->pinbits : nullptr,
                    h->grid ? nullptr : h->inv_mass, h->average ? 1 : 0, h->N, h->num_sms,
@@ -660,6 +682,7 @@ extern "C" int cs_read(cs_engine *h, int32_t id, void *dst) {
         case CS_BUF_VELOCITIES:
         case CS_BUF_PREV_POSITIONS:
         case CS_BUF_NORMALS: {
+            if (id == CS_BUF_NORMALS) flush_normals(h);
             const void *base = id == CS_BUF_NORMALS ? h->normals
                                : id == CS_BUF_PREV_POSITIONS ? h->state[1 - h->cur]
                                                              : h->state[h->cur];
@@ -712,6 +735,7 @@ extern "C" int cs_write(cs_engine *h, int32_t id, const void *src) {
         case CS_BUF_POSITIONS:
         case CS_BUF_VELOCITIES: {
             if (!src) return fail(CS_E_INVALID, "null source");
+            flush_normals(h);
             const int64_t o = id == CS_BUF_VELOCITIES ? 3 * P : 0;
             if (h->fp64) {
                 float *tmp;

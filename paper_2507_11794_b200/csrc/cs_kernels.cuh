@@ -167,6 +167,9 @@ void launch_csr_normals_f64(int64_t n, int64_t P, int64_t nc, const double *pos,
 // ---- launchers (defined in the .cu files) -------------------------------------
 void launch_grid_step(const StepParams &p, bool fixed, const float *src, float *dst,
                       const uint32_t *pinbits, const float *ext, cudaStream_t st);
+void launch_strip_step(const StepParams &p, bool fixed, bool normals, const float *src,
+                       float *dst, const uint32_t *pinbits, const float *ext, float *nrm,
+                       cudaStream_t st);
 void launch_grid_forces(const StepParams &p, const float *src, int32_t *forces, cudaStream_t st);
 void launch_grid_normals(const StepParams &p, bool exact, const float *state, float *nrm,
                          cudaStream_t st);

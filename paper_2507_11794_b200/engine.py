@@ -212,7 +212,7 @@ class Engine:
     def __init__(self, mesh, obstacle=None, params=None, device=None,
                  pair_budget: int = DEFAULT_PAIR_BUDGET, *, precision: str = "fast",
                  graph: bool = True, stream=None, cell_size: float | None = None,
-                 force_csr: bool = False):
+                 force_csr: bool = False, kernel: str = "strip"):
         if precision not in PRECISIONS:
             raise ValueError(f"precision must be one of {PRECISIONS}")
         self.mesh = mesh
@@ -284,6 +284,10 @@ class Engine:
             flags |= N.FLAG_NO_GRAPH
         if force_csr:
             flags |= N.FLAG_FORCE_CSR
+        if kernel not in ("strip", "tile"):
+            raise ValueError("kernel must be 'strip' (warp-strip, default) or 'tile'")
+        if kernel == "tile":
+            flags |= N.FLAG_TILE_KERNEL
         d.flags = flags
         if stencil is not None:
             d.nx, d.ny = stencil[0], stencil[1]
@@ -318,7 +322,11 @@ class Engine:
         d.substeps = int(p.substeps)
         d.cell_size = float(cell_size) if cell_size else 0.0
         if stream is not None:
-            d.stream = int(getattr(stream, "cuda_stream", stream))
+            handle = int(getattr(stream, "cuda_stream", stream))
+            if handle == 0:
+                raise ValueError("pass a non-default CUDA stream (the legacy default stream "
+                                 "handle 0 means 'let the engine create its own')")
+            d.stream = handle
         h = ctypes.c_void_p()
         N.check(self._lib.cs_create(ctypes.byref(d), ctypes.byref(h)))
         self._handle = h

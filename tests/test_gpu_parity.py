@@ -102,15 +102,28 @@ def test_fast_mode_100_steps_within_1e3_of_extent(config):
     assert np.abs(eng.read_normals() - so.normals).max() < 1e-3
 
 
-def test_fast_stencil_equals_fast_csr_bit_for_bit():
-    sc = P.build_scene(P.ScenarioConfig("hanging", (40, 33), dt=0.004))
-    a = P.Engine(sc.mesh, params=sc.params, precision="fast")
-    b = P.Engine(sc.mesh, params=sc.params, precision="fast", force_csr=True)
-    assert a.stencil and not b.stencil
-    a.step_frames(50)
-    b.step_frames(50)
-    np.testing.assert_array_equal(a.read_positions(), b.read_positions())
-    np.testing.assert_array_equal(a.read_velocities(), b.read_velocities())
+@pytest.mark.parametrize("shape", [(40, 33), (67, 130), (29, 29), (2, 5), (5, 2)])
+def test_grid_kernels_agree_with_csr(shape):
+    """strip kernel, tile kernel and generic CSR gather: bit-identical in
+    fixed point (integer sums), within 1e-6 of extent in the fast mode (the
+    float sum order differs between them)."""
+    sc = P.build_scene(P.ScenarioConfig("hanging", shape, dt=0.004))
+    for precision in ("fixed", "fast"):
+        engs = [P.Engine(sc.mesh, params=sc.params, precision=precision),
+                P.Engine(sc.mesh, params=sc.params, precision=precision, kernel="tile"),
+                P.Engine(sc.mesh, params=sc.params, precision=precision, force_csr=True)]
+        assert engs[0].stencil and not engs[2].stencil
+        for e in engs:
+            e.step_frames(50)
+        ref = engs[2]
+        for e in engs[:2]:
+            if precision == "fixed":
+                np.testing.assert_array_equal(e.read_positions(), ref.read_positions())
+                np.testing.assert_array_equal(e.read_velocities(), ref.read_velocities())
+                np.testing.assert_array_equal(e.read_normals(), ref.read_normals())
+            else:
+                np.testing.assert_allclose(e.read_positions(), ref.read_positions(), atol=1e-6)
+                np.testing.assert_allclose(e.read_normals(), ref.read_normals(), atol=1e-5)
 
 
 def test_graph_replay_equals_eager_launches():

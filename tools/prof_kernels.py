@@ -18,7 +18,8 @@ reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 t0 = time.time()
 sc = P.baseline_scene(cfg)
 t1 = time.time()
-stream = torch.cuda.current_stream()
+stream = torch.cuda.Stream()
+torch.cuda.set_stream(stream)
 eng = P.Engine(sc.mesh, sc.obstacle, sc.params, pair_budget=10**13, stream=stream.cuda_stream)
 t2 = time.time()
 print(f"{cfg}: scene {t1 - t0:.1f}s engine {t2 - t1:.1f}s nodes {sc.mesh.num_nodes}", flush=True)
