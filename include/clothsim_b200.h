@@ -64,6 +64,8 @@ extern "C" {
 #define CS_FLAG_TILE_KERNEL 64u     /* grid path: the shared-memory tile kernel
                                        (every node evaluates its 12 springs)
                                        instead of the warp-strip kernel */
+#define CS_FLAG_UNPACKED 128u       /* fast mode: the scalar warp-strip kernel
+                                       instead of the paired-fp32 (f32x2) one */
 
 typedef struct cs_engine cs_engine;
 

@@ -213,7 +213,8 @@ static void pass_force_integrate(cs_engine *h, bool fuse_normals = false) {
             // normals of the frame's starting state ride along in the first substep
             launch_strip_step(h->sp, h->fixed, fuse_normals && s == 0, (const float *)h->state[src],
                               (float *)h->state[dst], h->pinbits,
-                              h->has_ext ? (const float *)h->ext : nullptr, (float *)h->normals, h->st);
+                              h->has_ext ? (const float *)h->ext : nullptr, (float *)h->normals, h->st,
+                              !(h->flags & CS_FLAG_UNPACKED));
         } else if (h->grid) {
             launch_grid_step(h->sp, h->fixed, (const float *)h->state[src], (float *)h->state[dst],
                              h->pinbits, h->has_ext ? (const float *)h->ext : nullptr, h->st);

@@ -32,7 +32,8 @@ __device__ __forceinline__ void spring_fast(float dx, float dy, float dz, float 
     const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
     if (d2 >= 1e-24f) {
         const float inv = rsqrtf(d2);
-        const float len = d2 * inv;
+        const float l0 = d2 * inv;
+        const float len = fmaf(fmaf(-l0, l0, d2), 0.5f * inv, l0);  // Newton-refined |d|
         const float rel = fmaf(ux, dx, fmaf(uy, dy, uz * dz)) * inv;
         const float sc = fmaf(k, len - rest, c * rel) * inv;
         fx = fmaf(sc, dx, fx);
@@ -169,7 +170,10 @@ void launch_grid_step(const StepParams &p, bool fixed, const float *src, float *
                       const uint32_t *pinbits, const float *ext, cudaStream_t st);
 void launch_strip_step(const StepParams &p, bool fixed, bool normals, const float *src,
                        float *dst, const uint32_t *pinbits, const float *ext, float *nrm,
-                       cudaStream_t st);
+                       cudaStream_t st, bool packed = true);
+void launch_strip2_step(const StepParams &p, bool normals, const float *src, float *dst,
+                        const uint32_t *pinbits, const float *ext, float *nrm, cudaStream_t st);
+int strip2_rows(const StepParams &p);
 void launch_grid_forces(const StepParams &p, const float *src, int32_t *forces, cudaStream_t st);
 void launch_grid_normals(const StepParams &p, bool exact, const float *state, float *nrm,
                          cudaStream_t st);

@@ -37,7 +37,7 @@ namespace cs {
 
 constexpr int SW = 32;       // columns per warp (lanes)
 constexpr int SO = 28;       // output columns per warp
-constexpr int SH = 64;       // output rows per warp
+constexpr int SH_MAX = 64;   // output rows per warp (fewer when the grid is small)
 constexpr int SWPB = 4;      // warps per block
 
 struct N6 {
@@ -108,7 +108,10 @@ __device__ __forceinline__ V3<typename Acc<FIXED>::T> fwd(const N6 &a, const N6 
     } else {
         const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
         const float inv = rsqrtf(fmaxf(d2, 1e-30f));
-        const float len = d2 * inv;
+        // one Newton step on the residual makes |d| (nearly) correctly
+        // rounded, so a spring at rest sees exactly zero stretch
+        const float l0 = d2 * inv;
+        const float len = fmaf(fmaf(-l0, l0, d2), 0.5f * inv, l0);
         const float rel = fmaf(ux, dx, fmaf(uy, dy, uz * dz)) * inv;
         float sc = fmaf(k, len - rest, c * rel) * inv;
         sc = (ok && d2 >= 1e-24f) ? sc : 0.f;  // solver.py:111-113 skips length < 1e-12
@@ -160,9 +163,9 @@ k_strip_step(const StepParams p, const float *__restrict__ src, float *__restric
     const int warp = blockIdx.x * SWPB + (threadIdx.x >> 5);
     const int strips_x = (p.nx + SO - 1) / SO;
     const int sx = warp % strips_x, sy = warp / strips_x;
-    const int y0 = sy * SH;
+    const int y0 = sy * p.strip_h;
     if (y0 >= p.ny) return;  // whole warp exits together
-    const int y1 = min(y0 + SH, p.ny);
+    const int y1 = min(y0 + p.strip_h, p.ny);
     const int i = sx * SO - 2 + lane;
     const bool col_ok = (i >= 0) & (i < p.nx);
     const bool out_lane = (lane >= 2) & (lane < 30) & col_ok;
@@ -279,16 +282,27 @@ k_strip_step(const StepParams p, const float *__restrict__ src, float *__restric
 
 void launch_strip_step(const StepParams &p, bool fixed, bool normals, const float *src,
                        float *dst, const uint32_t *pinbits, const float *ext, float *nrm,
-                       cudaStream_t st) {
-    const int strips = ((p.nx + SO - 1) / SO) * ((p.ny + SH - 1) / SH);
-    const unsigned blocks = (unsigned)((strips + SWPB - 1) / SWPB);
+                       cudaStream_t st, bool packed) {
+    if (!fixed && packed) {  // production fast path: cs_strip2.cu
+        launch_strip2_step(p, normals, src, dst, pinbits, ext, nrm, st);
+        return;
+    }
+    // Tall strips amortise the 2-row vertical halo; small grids get shorter
+    // strips so that >= ~16 warps per SM (148 SMs) are resident.
+    const int sxn = (p.nx + SO - 1) / SO;
     const dim3 block(SW * SWPB);
+    int sh = SH_MAX;
+    while (sh > 8 && (int64_t)sxn * ((p.ny + sh - 1) / sh) < 148 * 16) sh /= 2;
+    StepParams q = p;
+    q.strip_h = sh;
+    const int64_t strips = (int64_t)sxn * ((p.ny + sh - 1) / sh);
+    const unsigned blocks = (unsigned)((strips + SWPB - 1) / SWPB);
     if (fixed) {
-        if (normals) k_strip_step<true, true><<<blocks, block, 0, st>>>(p, src, dst, pinbits, ext, nrm);
-        else k_strip_step<true, false><<<blocks, block, 0, st>>>(p, src, dst, pinbits, ext, nrm);
+        if (normals) k_strip_step<true, true><<<blocks, block, 0, st>>>(q, src, dst, pinbits, ext, nrm);
+        else k_strip_step<true, false><<<blocks, block, 0, st>>>(q, src, dst, pinbits, ext, nrm);
     } else {
-        if (normals) k_strip_step<false, true><<<blocks, block, 0, st>>>(p, src, dst, pinbits, ext, nrm);
-        else k_strip_step<false, false><<<blocks, block, 0, st>>>(p, src, dst, pinbits, ext, nrm);
+        if (normals) k_strip_step<false, true><<<blocks, block, 0, st>>>(q, src, dst, pinbits, ext, nrm);
+        else k_strip_step<false, false><<<blocks, block, 0, st>>>(q, src, dst, pinbits, ext, nrm);
     }
 }
 

@@ -284,10 +284,13 @@ class Engine:
             flags |= N.FLAG_NO_GRAPH
         if force_csr:
             flags |= N.FLAG_FORCE_CSR
-        if kernel not in ("strip", "tile"):
-            raise ValueError("kernel must be 'strip' (warp-strip, default) or 'tile'")
+        if kernel not in ("strip", "strip1", "tile"):
+            raise ValueError("kernel must be 'strip' (paired-fp32 warp strips, default), "
+                             "'strip1' (scalar warp strips) or 'tile' (shared-memory tiles)")
         if kernel == "tile":
             flags |= N.FLAG_TILE_KERNEL
+        if kernel == "strip1":
+            flags |= N.FLAG_UNPACKED
         d.flags = flags
         if stencil is not None:
             d.nx, d.ny = stencil[0], stencil[1]
@@ -331,7 +334,7 @@ class Engine:
         N.check(self._lib.cs_create(ctypes.byref(d), ctypes.byref(h)))
         self._handle = h
         self.kparams = d  # the baked parameter block (engine.py:274-285 KernelParams)
-        self.stencil = stencil is not None
+        self.stencil = stencil is not None and not force_csr and precision != "fp64"
         self.frame_count = 0
         self.buffers = PipelineBuffers(self)
         self._has_obstacle = has_obs
