@@ -64,8 +64,9 @@ extern "C" {
 #define CS_FLAG_TILE_KERNEL 64u     /* grid path: the shared-memory tile kernel
                                        (every node evaluates its 12 springs)
                                        instead of the warp-strip kernel */
-#define CS_FLAG_UNPACKED 128u       /* fast mode: the scalar warp-strip kernel
-                                       instead of the paired-fp32 (f32x2) one */
+#define CS_FLAG_PAIRED 128u         /* fast mode: the experimental paired-column
+                                       f32x2 warp-strip kernel (cs_strip2.cu)
+                                       instead of the scalar one */
 
 typedef struct cs_engine cs_engine;
 

@@ -90,14 +90,24 @@ OR_EXPORT i64 or_sol_forces(i64 n, i64 ns, const i32 *sidx, const double *rest,
          * by spring id.  Each node then receives exactly the serial loop's
          * sequence of adds (0 + g_s1 - g_s2 ...), so the result is
          * bit-identical to the serial scatter for any thread count. */
-        i64 *off = (i64 *)calloc(n + 1, sizeof(i64));
-        i64 *ent = (i64 *)malloc(sizeof(i64) * 2 * (ns > 0 ? ns : 1));
-        for (i64 s = 0; s < ns; ++s) { off[sidx[2 * s] + 1]++; off[sidx[2 * s + 1] + 1]++; }
-        for (i64 i = 0; i < n; ++i) off[i + 1] += off[i];
-        i64 *fill = (i64 *)malloc(sizeof(i64) * (n > 0 ? n : 1));
-        memcpy(fill, off, sizeof(i64) * n);
-        for (i64 s = 0; s < ns; ++s) { ent[fill[sidx[2 * s]]++] = s; ent[fill[sidx[2 * s + 1]]++] = s; }
-        free(fill);
+        /* the incidence CSR depends only on the spring table: cache it */
+        static const i32 *c_sidx = NULL;
+        static i64 c_ns = -1, c_n = -1, c_sig = 0;
+        static i64 *off = NULL, *ent = NULL;
+        i64 sig = ns > 0 ? ((i64)sidx[0] * 31 + sidx[2 * ns - 1]) * 131 + sidx[ns] : 0;
+        if (c_sidx != sidx || c_ns != ns || c_n != n || c_sig != sig) {
+            free(off);
+            free(ent);
+            off = (i64 *)calloc(n + 1, sizeof(i64));
+            ent = (i64 *)malloc(sizeof(i64) * 2 * (ns > 0 ? ns : 1));
+            for (i64 s = 0; s < ns; ++s) { off[sidx[2 * s] + 1]++; off[sidx[2 * s + 1] + 1]++; }
+            for (i64 i = 0; i < n; ++i) off[i + 1] += off[i];
+            i64 *fill = (i64 *)malloc(sizeof(i64) * (n > 0 ? n : 1));
+            memcpy(fill, off, sizeof(i64) * n);
+            for (i64 s = 0; s < ns; ++s) { ent[fill[sidx[2 * s]]++] = s; ent[fill[sidx[2 * s + 1]]++] = s; }
+            free(fill);
+            c_sidx = sidx; c_ns = ns; c_n = n; c_sig = sig;
+        }
         i64 degs = 0;
 #pragma omp parallel for num_threads(nt) schedule(static) reduction(+ : degs)
         for (i64 v = 0; v < n; ++v) {
@@ -120,8 +130,6 @@ OR_EXPORT i64 or_sol_forces(i64 n, i64 ns, const i32 *sidx, const double *rest,
             f[3 * v] = fx; f[3 * v + 1] = fy; f[3 * v + 2] = fz;
         }
         degenerate = degs;
-        free(off);
-        free(ent);
     }
     /* forces += masses[:, None] * gravity; forces += masses * ext; pinned = 0 */
     for (i64 i = 0; i < n; ++i) {

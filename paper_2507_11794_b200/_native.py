@@ -13,7 +13,8 @@ import os
 from .errors import AdapterUnavailable, CapacityError, CollisionBudgetError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libclothsim_b200.so")
+# CLOTHSIM_LIB selects an alternative in-tree build (kernel A/B experiments)
+LIB_PATH = os.environ.get("CLOTHSIM_LIB") or os.path.join(HERE, "_lib", "libclothsim_b200.so")
 
 ABI_VERSION = 1
 CS_OK, CS_E_INVALID, CS_E_CAPACITY, CS_E_BUDGET, CS_E_NODEVICE, CS_E_CUDA = 0, -1, -2, -3, -4, -5
@@ -25,7 +26,7 @@ FLAG_FP64 = 8
 FLAG_NO_GRAPH = 16
 FLAG_FORCE_CSR = 32
 FLAG_TILE_KERNEL = 64
-FLAG_UNPACKED = 128
+FLAG_PAIRED = 128
 
 BUF_POSITIONS, BUF_VELOCITIES, BUF_NORMALS, BUF_PREV_POSITIONS = 0, 1, 2, 3
 BUF_FORCES_RAW, BUF_ACCUMULATOR, BUF_COUNTS, BUF_EXT_ACCEL = 4, 5, 6, 7

@@ -214,7 +214,7 @@ static void pass_force_integrate(cs_engine *h, bool fuse_normals = false) {
             launch_strip_step(h->sp, h->fixed, fuse_normals && s == 0, (const float *)h->state[src],
                               (float *)h->state[dst], h->pinbits,
                               h->has_ext ? (const float *)h->ext : nullptr, (float *)h->normals, h->st,
-                              !(h->flags & CS_FLAG_UNPACKED));
+                              (h->flags & CS_FLAG_PAIRED) != 0);
         } else if (h->grid) {
             launch_grid_step(h->sp, h->fixed, (const float *)h->state[src], (float *)h->state[dst],
                              h->pinbits, h->has_ext ? (const float *)h->ext : nullptr, h->st);

@@ -170,7 +170,7 @@ void launch_grid_step(const StepParams &p, bool fixed, const float *src, float *
                       const uint32_t *pinbits, const float *ext, cudaStream_t st);
 void launch_strip_step(const StepParams &p, bool fixed, bool normals, const float *src,
                        float *dst, const uint32_t *pinbits, const float *ext, float *nrm,
-                       cudaStream_t st, bool packed = true);
+                       cudaStream_t st, bool packed = false);
 void launch_strip2_step(const StepParams &p, bool normals, const float *src, float *dst,
                         const uint32_t *pinbits, const float *ext, float *nrm, cudaStream_t st);
 int strip2_rows(const StepParams &p);

@@ -284,13 +284,13 @@ class Engine:
             flags |= N.FLAG_NO_GRAPH
         if force_csr:
             flags |= N.FLAG_FORCE_CSR
-        if kernel not in ("strip", "strip1", "tile"):
-            raise ValueError("kernel must be 'strip' (paired-fp32 warp strips, default), "
-                             "'strip1' (scalar warp strips) or 'tile' (shared-memory tiles)")
+        if kernel not in ("strip", "pair", "tile"):
+            raise ValueError("kernel must be 'strip' (warp strips, default), 'pair' "
+                             "(paired-column f32x2 warp strips) or 'tile' (shared-memory tiles)")
         if kernel == "tile":
             flags |= N.FLAG_TILE_KERNEL
-        if kernel == "strip1":
-            flags |= N.FLAG_UNPACKED
+        if kernel == "pair":
+            flags |= N.FLAG_PAIRED
         d.flags = flags
         if stencil is not None:
             d.nx, d.ny = stencil[0], stencil[1]

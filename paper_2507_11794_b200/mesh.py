@@ -229,6 +229,34 @@ def generate_cloth_grid(nx: int, ny: int, width: float = 1.0, height: float = 1.
                      triangles=grid_triangles(nx, ny))
 
 
+def grid_band(nx: int, ny: int, j0: int, j1: int, width: float = 1.0, height: float = 1.0,
+              total_mass: float = None, pinned_rows=None) -> ClothMesh:
+    """Rows [j0, j1) of generate_cloth_grid(nx, ny, ...) as a stand-alone
+    ClothMesh: same node coordinates, masses and pins as the global grid, the
+    grid topology of an nx x (j1-j0) sheet, and rest lengths computed from
+    the same global coordinates -- so a row band steps exactly like the
+    corresponding rows of the whole cloth (multi-GPU row bands, bands.py)."""
+    if not (0 <= j0 < j1 <= ny) or j1 - j0 < 2:
+        raise ValueError(f"band [{j0}, {j1}) outside a grid of {ny} rows")
+    n = nx * ny
+    if total_mass is None:
+        total_mass = 0.05 * n
+    lny = j1 - j0
+    positions = np.zeros((nx * lny, 3), dtype=np.float64)
+    positions[:, 0] = np.tile(np.linspace(0.0, width, nx), lny)
+    positions[:, 2] = np.repeat(np.linspace(0.0, height, ny)[j0:j1], nx)
+    masses = np.full(nx * lny, total_mass / n, dtype=np.float64)
+    pinned = np.zeros(nx * lny, dtype=bool)
+    for j in _resolve_pinned_rows(pinned_rows, ny):
+        if j0 <= j < j1:
+            pinned[(j - j0) * nx:(j - j0 + 1) * nx] = True
+    springs, kinds = grid_springs(nx, lny)
+    rest = np.linalg.norm(positions[springs[:, 1]] - positions[springs[:, 0]], axis=1)
+    return ClothMesh(nx=nx, ny=lny, positions=positions, masses=masses, pinned=pinned,
+                     spring_indices=springs, spring_rest_lengths=rest, spring_kinds=kinds,
+                     triangles=grid_triangles(nx, lny))
+
+
 def _resolve_pinned_rows(pinned_rows, ny: int):
     if pinned_rows is None or (isinstance(pinned_rows, str) and pinned_rows == "none"):
         return []
