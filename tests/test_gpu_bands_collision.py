@@ -1,0 +1,64 @@
+"""GPU: row bands (several bands on one GPU, halos swapped by the same row
+plans the NCCL path uses) and the full-size collision scene."""
+
+import numpy as np
+import pytest
+
+import paper_2507_11794_b200 as P
+from paper_2507_11794_b200.bands import BandedEngine
+from paper_2507_11794_b200.scenes import CONTACT_DT, NODE_MASS, stable_coefficients
+
+pytestmark = pytest.mark.gpu
+
+
+def _swap(bands):
+    """In-process equivalent of exchange_halos for bands on one device."""
+    planes = [b.planes() for b in bands]
+    for r in range(len(bands) - 1):
+        up, dn = bands[r].plan, bands[r + 1].plan
+        for q in range(6):
+            a, b = up.send_down, dn.recv_up
+            planes[r + 1][q][b[0]:b[1]].copy_(planes[r][q][a[0]:a[1]])
+            a, b = dn.send_up, up.recv_down
+            planes[r][q][b[0]:b[1]].copy_(planes[r + 1][q][a[0]:a[1]])
+
+
+@pytest.mark.parametrize("world,precision", [(2, "fast"), (3, "fast"), (4, "fixed")])
+def test_banded_run_is_bit_identical_to_one_engine(world, precision):
+    import torch
+
+    n = 160
+    k, c = stable_coefficients(NODE_MASS, CONTACT_DT)
+    params = P.SimParams(dt=CONTACT_DT, stiffness=k, damping=c)
+    whole = P.Engine(P.baseline_scene("C2").mesh if n == 800 else
+                     P.build_scene(P.ScenarioConfig("hanging", (n, n), dt=CONTACT_DT)).mesh,
+                     params=params, precision=precision)
+    bands = [BandedEngine(n, n, params, r, world) for r in range(world)]
+    for b in bands:
+        b.engine.close()
+        b.engine = P.Engine(b.mesh, params=params, precision=precision)
+    for _ in range(25):
+        whole.step()
+        for b in bands:
+            b.engine.step()
+        torch.cuda.synchronize()
+        _swap(bands)
+        torch.cuda.synchronize()
+    got = np.concatenate([b.owned_positions() for b in bands])
+    np.testing.assert_array_equal(got, whole.read_positions())
+
+
+def test_c3_drapes_finite_with_contacts_in_both_modes():
+    sc = P.baseline_scene("C3")
+    hits = {}
+    for precision in ("fast", "fixed"):
+        eng = P.Engine(sc.mesh, sc.obstacle, sc.params, pair_budget=10**13, precision=precision)
+        eng.step_frames(400)
+        pos = eng.read_positions()
+        assert np.isfinite(pos).all()
+        hits[precision] = eng.stats()["hit_counter"]
+        assert hits[precision] > 100_000
+        # nobody tunnels far into the sphere (radius 0.3, margin 1e-3)
+        r = np.linalg.norm(pos.astype(np.float64), axis=1)
+        assert (r > 0.27).mean() > 0.999
+    assert abs(hits["fast"] - hits["fixed"]) / hits["fixed"] < 0.05
