@@ -64,6 +64,8 @@ extern "C" {
 #define CS_FLAG_TILE_KERNEL 64u     /* grid path: the shared-memory tile kernel
                                        (every node evaluates its 12 springs)
                                        instead of the warp-strip kernel */
+#define CS_FLAG_THREAD_NARROW 256u  /* collision narrow phase: one thread per
+                                       query instead of one warp per query */
 #define CS_FLAG_PAIRED 128u         /* fast mode: the experimental paired-column
                                        f32x2 warp-strip kernel (cs_strip2.cu)
                                        instead of the scalar one */

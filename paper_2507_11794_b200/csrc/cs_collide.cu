@@ -250,6 +250,8 @@ __global__ void k_cell_ranges(const uint32_t *__restrict__ keys, int64_t n,
 
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
+void launch_tri_boxes(int64_t nt, const float *corners, float *box, cudaStream_t st);
+
 int build_broadphase(BroadPhase &bp, const float *d_corners, int64_t nt, const float *h_corners,
                      float cell_size, cudaStream_t st) {
     // grid over the obstacle's bounding box (host: static data, computed once)
@@ -267,7 +269,9 @@ int build_broadphase(BroadPhase &bp, const float *d_corners, int64_t nt, const f
         mean_ext += fmax(fmax(b[0] - a[0], b[1] - a[1]), b[2] - a[2]);
     }
     mean_ext /= (double)(nt > 0 ? nt : 1);
-    float cs_ = cell_size > 0.f ? cell_size : (float)(2.0 * mean_ext);
+    // cells about one triangle box across: C3 sweep (tools/c3_cells.py) put
+    // the optimum near 1x the mean extent (2x was 40% slower)
+    float cs_ = cell_size > 0.f ? cell_size : (float)(1.0 * mean_ext);
     if (!(cs_ > 0.f)) cs_ = 1.0f;
     int dims[3];
     for (;;) {
@@ -322,6 +326,8 @@ int build_broadphase(BroadPhase &bp, const float *d_corners, int64_t nt, const f
     cudaFree(counts);
     cudaFree(offsets);
     cudaFree(tk);
+    cudaMalloc(&bp.tri_box, 6 * (nt > 0 ? nt : 1) * sizeof(float));
+    launch_tri_boxes(nt, d_corners, bp.tri_box, st);
     cudaFree(tv);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
@@ -331,6 +337,7 @@ void free_broadphase(BroadPhase &bp) {
     cudaFree(bp.cell_end);
     cudaFree(bp.cell_keys);
     cudaFree(bp.cell_tris);
+    cudaFree(bp.tri_box);
     bp = BroadPhase();
 }
 
@@ -604,9 +611,170 @@ __global__ void k_rebuild_touched(const CollideArgs A, int64_t n_rows, int64_t n
     }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-per-query narrow phase ("one warp per cell-candidate batch").  A warp
+// takes one query (cloth edge for pass A, cloth triangle for pass B); its
+// lanes read up to 32 of the query's grid cells at a time, a warp-shuffle
+// inclusive scan flattens the cells' candidate lists, and every lane takes
+// candidates t = lane, lane+32, ... (owner cell found by a 5-step shuffle
+// binary search).  Divergence between queries with few and many candidates
+// -- the cost of the thread-per-query kernels above -- disappears; queries
+// whose box misses the obstacle leave after one test.  Same box test, dedup
+// rule, predicate and accumulation as the thread-per-query kernels.
+// ---------------------------------------------------------------------------
+template <int PASS>  // 0: cloth edges vs obstacle triangles, 1: obstacle edges vs cloth triangles
+__global__ void __launch_bounds__(256)
+k_detect_warp(const CollideArgs A, const GridDesc g, const uint32_t *__restrict__ cbeg,
+              const uint32_t *__restrict__ cend, const uint32_t *__restrict__ ctri,
+              const float *__restrict__ tbox, const float *__restrict__ corners,
+              const float *__restrict__ normals, const int32_t *__restrict__ items, int64_t nq) {
+    const int lane = threadIdx.x & 31;
+    const int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    uint32_t hits = 0;
+    if (q < nq) {  // warp-uniform
+        float v[3][3];
+        int64_t nid[3];
+        const int nv = PASS == 0 ? 2 : 3;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if (k < nv) {
+                nid[k] = items[nv * q + k];
+                load_pos(A, nid[k], v[k]);
+            }
+        }
+        float lo[3], hi[3], clo[3], chi[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            if (PASS == 0) {  // kernels.py:55-59: padded segment box
+                lo[d] = fsub(fminf(v[0][d], v[1][d]), A.pad);
+                hi[d] = fadd(fmaxf(v[0][d], v[1][d]), A.pad);
+            } else {          // cloth triangle box, queried padded by 2*pad
+                clo[d] = fminf(fminf(v[0][d], v[1][d]), v[2][d]);
+                chi[d] = fmaxf(fmaxf(v[0][d], v[1][d]), v[2][d]);
+                lo[d] = clo[d] - 2.0f * A.pad;
+                hi[d] = chi[d] + 2.0f * A.pad;
+            }
+        }
+        if (g.overlaps(lo, hi)) {
+            int a[3], b[3];
+            g.cell_range(lo, hi, a, b);
+            const int ex = b[0] - a[0] + 1, ey = b[1] - a[1] + 1, ez = b[2] - a[2] + 1;
+            const int ncell = ex * ey * ez;
+            for (int c0 = 0; c0 < ncell; c0 += 32) {
+                const int c = c0 + lane;
+                int cx = 0, cy = 0, cz = 0;
+                uint32_t beg = 0, cnt = 0;
+                if (c < ncell) {
+                    cx = a[0] + c % ex;
+                    cy = a[1] + (c / ex) % ey;
+                    cz = a[2] + c / (ex * ey);
+                    const uint32_t key = g.key(cx, cy, cz);
+                    beg = cbeg[key];
+                    cnt = cend[key] - beg;
+                }
+                const uint32_t incl = warp_incl_scan(cnt);
+                const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+                for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+                    const uint32_t t = t0 + lane;
+                    // owner lane: smallest L with incl[L] > t
+                    int o = 0;
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1) {
+                        const uint32_t probe = __shfl_sync(0xffffffffu, incl, o + step - 1);
+                        if (probe <= t) o += step;
+                    }
+                    const uint32_t ob = __shfl_sync(0xffffffffu, beg, o);
+                    const uint32_t oi = __shfl_sync(0xffffffffu, incl, o);
+                    const uint32_t oc = __shfl_sync(0xffffffffu, cnt, o);
+                    const int ox = __shfl_sync(0xffffffffu, cx, o);
+                    const int oy = __shfl_sync(0xffffffffu, cy, o);
+                    const int oz = __shfl_sync(0xffffffffu, cz, o);
+                    if (t >= total) continue;
+                    const uint32_t tri = ctri[ob + (t - (oi - oc))];
+                    const float *tb = tbox + 6 * (int64_t)tri;
+                    const float tlo[3] = {tb[0], tb[1], tb[2]}, thi[3] = {tb[3], tb[4], tb[5]};
+                    if (!box_overlap(lo, hi, tlo, thi)) continue;
+                    // dedup: the minimum corner of the intersection lies in this cell
+                    if (g.cell_of(fmaxf(lo[0], tlo[0]), 0) != ox || g.cell_of(fmaxf(lo[1], tlo[1]), 1) != oy ||
+                        g.cell_of(fmaxf(lo[2], tlo[2]), 2) != oz)
+                        continue;
+                    const float *cr = corners + 9 * (int64_t)tri;
+                    const float *nrm = normals + 3 * (int64_t)tri;
+                    if (PASS == 0) {
+                        float pt[3];
+                        if (!seg_tri(v[0], v[1], cr, cr + 3, cr + 6, A.eps, pt)) continue;
+                        ++hits;
+                        const float sa = dot3x(fsub(v[0][0], pt[0]), fsub(v[0][1], pt[1]),
+                                               fsub(v[0][2], pt[2]), nrm[0], nrm[1], nrm[2]);
+                        const float sb = dot3x(fsub(v[1][0], pt[0]), fsub(v[1][1], pt[1]),
+                                               fsub(v[1][2], pt[2]), nrm[0], nrm[1], nrm[2]);
+                        const float sign = np_max(sa, sb) >= 0.f ? 1.f : -1.f;
+                        const float on[3] = {fmul(nrm[0], sign), fmul(nrm[1], sign), fmul(nrm[2], sign)};
+                        accumulate(A, nid[0], v[0], pt, on);
+                        accumulate(A, nid[1], v[1], pt, on);
+                    } else {
+                        for (int slot = 0; slot < 3; ++slot) {
+                            const float *st = cr + 3 * slot;
+                            const float *en = cr + 3 * ((slot + 1) % 3);
+                            float elo[3], ehi[3];
+#pragma unroll
+                            for (int d = 0; d < 3; ++d) {
+                                elo[d] = fsub(fminf(st[d], en[d]), A.pad);
+                                ehi[d] = fadd(fmaxf(st[d], en[d]), A.pad);
+                            }
+                            if (!box_overlap(elo, ehi, clo, chi)) continue;
+                            float pt[3];
+                            if (!seg_tri(st, en, v[0], v[1], v[2], A.eps, pt)) continue;
+                            ++hits;
+                            const float t0s = dot3x(fsub(v[0][0], pt[0]), fsub(v[0][1], pt[1]),
+                                                    fsub(v[0][2], pt[2]), nrm[0], nrm[1], nrm[2]);
+                            const float t1s = dot3x(fsub(v[1][0], pt[0]), fsub(v[1][1], pt[1]),
+                                                    fsub(v[1][2], pt[2]), nrm[0], nrm[1], nrm[2]);
+                            const float t2s = dot3x(fsub(v[2][0], pt[0]), fsub(v[2][1], pt[1]),
+                                                    fsub(v[2][2], pt[2]), nrm[0], nrm[1], nrm[2]);
+                            const float sign = fadd(fadd(t0s, t1s), t2s) >= 0.f ? 1.f : -1.f;
+                            const float on[3] = {fmul(nrm[0], sign), fmul(nrm[1], sign), fmul(nrm[2], sign)};
+                            accumulate(A, nid[0], v[0], pt, on);
+                            accumulate(A, nid[1], v[1], pt, on);
+                            accumulate(A, nid[2], v[2], pt, on);
+                        }
+                    }
+                }
+            }
+        }
+    }
+    count_hits(A.frame_hits, hits);
+}
+
+__global__ void k_tri_boxes(int64_t nt, const float *__restrict__ corners, float *__restrict__ box) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    float lo[3], hi[3];
+    tri_box(corners + 9 * t, lo, hi);
+    for (int d = 0; d < 3; ++d) {
+        box[6 * t + d] = lo[d];
+        box[6 * t + 3 + d] = hi[d];
+    }
+}
+
+void launch_tri_boxes(int64_t nt, const float *corners, float *box, cudaStream_t st) {
+    if (nt > 0) k_tri_boxes<<<nblk(nt, 256), 256, 0, st>>>(nt, corners, box);
+}
+
 void launch_detect(const CollideArgs &A, const BroadPhase &bp, const float *corners,
                    const float *normals, const int32_t *edges, int64_t ne, const int32_t *tris,
                    int64_t nc, cudaStream_t st) {
+    if (bp.warp_per_query) {
+        if (ne > 0)
+            k_detect_warp<0><<<nblk(ne * 32, 256), 256, 0, st>>>(A, bp.grid, bp.cell_begin, bp.cell_end,
+                                                                 bp.cell_tris, bp.tri_box, corners,
+                                                                 normals, edges, ne);
+        if (nc > 0)
+            k_detect_warp<1><<<nblk(nc * 32, 256), 256, 0, st>>>(A, bp.grid, bp.cell_begin, bp.cell_end,
+                                                                 bp.cell_tris, bp.tri_box, corners,
+                                                                 normals, tris, nc);
+        return;
+    }
     if (ne > 0)
         k_detect_cloth_edges<<<nblk(ne, 256), 256, 0, st>>>(A, bp.grid, bp.cell_begin, bp.cell_end,
                                                              bp.cell_tris, corners, normals, edges, ne);

@@ -212,7 +212,7 @@ class Engine:
     def __init__(self, mesh, obstacle=None, params=None, device=None,
                  pair_budget: int = DEFAULT_PAIR_BUDGET, *, precision: str = "fast",
                  graph: bool = True, stream=None, cell_size: float | None = None,
-                 force_csr: bool = False, kernel: str = "strip"):
+                 force_csr: bool = False, kernel: str = "strip", narrow: str = "warp"):
         if precision not in PRECISIONS:
             raise ValueError(f"precision must be one of {PRECISIONS}")
         self.mesh = mesh
@@ -289,6 +289,10 @@ class Engine:
                              "(paired-column f32x2 warp strips) or 'tile' (shared-memory tiles)")
         if kernel == "tile":
             flags |= N.FLAG_TILE_KERNEL
+        if narrow not in ("warp", "thread"):
+            raise ValueError("narrow must be 'warp' (warp per query) or 'thread'")
+        if narrow == "thread":
+            flags |= N.FLAG_THREAD_NARROW
         if kernel == "pair":
             flags |= N.FLAG_PAIRED
         d.flags = flags

@@ -137,6 +137,19 @@ def test_grid_kernels_agree_with_csr(shape):
                 np.testing.assert_allclose(e.read_normals(), ref.read_normals(), atol=1e-5)
 
 
+@pytest.mark.parametrize("narrow", ["warp", "thread"])
+@pytest.mark.parametrize("cell", [None, 0.02, 0.003])
+def test_narrow_phase_mappings_and_cell_sizes_are_bit_identical(narrow, cell):
+    """The hit set may not depend on how candidates are found."""
+    g, ref = _run_golden("traj_drop10.npz", "fixed")
+    _, eng = _run_golden("traj_drop10.npz", "fixed", narrow=narrow, cell_size=cell)
+    for f in range(1, 61):
+        eng.step()
+        if f in (20, 40, 60):
+            np.testing.assert_array_equal(eng.read_positions(), g[f"eng_pos_{f}"])
+    assert eng.stats()["hit_counter"] == int(g["eng_hits"].sum())
+
+
 def test_graph_replay_equals_eager_launches():
     g, a = _run_golden("traj_drop10.npz", "fixed")
     _, b = _run_golden("traj_drop10.npz", "fixed", graph=False)
