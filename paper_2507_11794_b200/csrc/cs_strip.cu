@@ -283,8 +283,8 @@ k_strip_step(const StepParams p, const float *__restrict__ src, float *__restric
 void launch_strip_step(const StepParams &p, bool fixed, bool normals, const float *src,
                        float *dst, const uint32_t *pinbits, const float *ext, float *nrm,
                        cudaStream_t st, bool packed) {
-    if (!fixed && packed) {  // production fast path: cs_strip2.cu
-        launch_strip2_step(p, normals, src, dst, pinbits, ext, nrm, st);
+    if (!fixed && packed) {  // paired-column f32x2 kernel: cs_pair3.cu
+        launch_pair3_step(p, normals, src, dst, pinbits, ext, nrm, st);
         return;
     }
     // Tall strips amortise the 2-row vertical halo; small grids get shorter

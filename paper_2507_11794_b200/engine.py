@@ -212,7 +212,7 @@ class Engine:
     def __init__(self, mesh, obstacle=None, params=None, device=None,
                  pair_budget: int = DEFAULT_PAIR_BUDGET, *, precision: str = "fast",
                  graph: bool = True, stream=None, cell_size: float | None = None,
-                 force_csr: bool = False, kernel: str = "strip", narrow: str = "warp"):
+                 force_csr: bool = False, kernel: str = "pair", narrow: str = "warp"):
         if precision not in PRECISIONS:
             raise ValueError(f"precision must be one of {PRECISIONS}")
         self.mesh = mesh

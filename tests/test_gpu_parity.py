@@ -122,7 +122,7 @@ def test_grid_kernels_agree_with_csr(shape):
                 P.Engine(sc.mesh, params=sc.params, precision=precision, kernel="tile"),
                 P.Engine(sc.mesh, params=sc.params, precision=precision, force_csr=True)]
         if precision == "fast":
-            engs.append(P.Engine(sc.mesh, params=sc.params, precision=precision, kernel="pair"))
+            engs.append(P.Engine(sc.mesh, params=sc.params, precision=precision, kernel="strip"))
         assert engs[0].stencil and not engs[2].stencil
         for e in engs:
             e.step_frames(50)
