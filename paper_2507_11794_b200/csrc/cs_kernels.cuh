@@ -171,9 +171,6 @@ void launch_grid_step(const StepParams &p, bool fixed, const float *src, float *
 void launch_strip_step(const StepParams &p, bool fixed, bool normals, const float *src,
                        float *dst, const uint32_t *pinbits, const float *ext, float *nrm,
                        cudaStream_t st, bool packed = false);
-void launch_strip2_step(const StepParams &p, bool normals, const float *src, float *dst,
-                        const uint32_t *pinbits, const float *ext, float *nrm, cudaStream_t st);
-int strip2_rows(const StepParams &p);
 void launch_pair3_step(const StepParams &p, bool normals, const float *src, float *dst,
                        const uint32_t *pinbits, const float *ext, float *nrm, cudaStream_t st);
 void launch_grid_forces(const StepParams &p, const float *src, int32_t *forces, cudaStream_t st);
