@@ -64,6 +64,11 @@ extern "C" {
 #define CS_FLAG_TILE_KERNEL 64u     /* grid path: the shared-memory tile kernel
                                        (every node evaluates its 12 springs)
                                        instead of the warp-strip kernel */
+#define CS_FLAG_SPLIT_NORMALS 512u  /* grid path: a stand-alone normals kernel
+                                       after each frame instead of fusing the
+                                       previous frame's normals into the step */
+#define CS_FLAG_FUSE_NORMALS 1024u  /* grid path: always fuse (default: fused
+                                       up to 2M nodes, split above) */
 #define CS_FLAG_THREAD_NARROW 256u  /* collision narrow phase: one thread per
                                        query instead of one warp per query */
 #define CS_FLAG_PAIRED 128u         /* fast mode: the experimental paired-column

@@ -81,6 +81,19 @@ struct cs_engine {
 
     bool has_obstacle = false;
     bool strip = true;          // grid path uses the warp-strip kernel (cs_strip.cu)
+    // The strip kernel can compute the previous frame's normals in the same
+    // pass (fused: one launch per frame, 60 B/node) or a stand-alone normals
+    // kernel can follow it (split: 72 B/node).  Measured on B200: fused wins
+    // while a frame is latency-bound (C2, 640K nodes: 24.6 vs 28.7 us), split
+    // wins once it is throughput-bound (C5, 16.8M: 330 vs 343 us) -- the fused
+    // kernel needs 168 registers, the pair 128 + 88.  Default: fused up to
+    // 2M nodes; CS_FLAG_FUSE_NORMALS / CS_FLAG_SPLIT_NORMALS force a choice.
+    bool fuse_normals() const {
+        if (!(grid && strip)) return false;
+        if (flags & CS_FLAG_SPLIT_NORMALS) return false;
+        if (flags & CS_FLAG_FUSE_NORMALS) return true;
+        return fixed || !(flags & CS_FLAG_PAIRED) || N <= (int64_t)1 << 21;
+    }
     bool normals_stale = false; // normals buffer holds the previous frame's (fused)
     float *corners = nullptr, *onormals = nullptr;
     BroadPhase bp;
@@ -123,7 +136,7 @@ struct cs_engine {
     int kernels_per_frame() const {
         int k = substeps;  // one fused force+integrate launch per substep
         if (has_obstacle) k += 2 /*detect*/ + 2 /*respond + frame_end*/;
-        if (!(grid && strip)) k += grid ? 1 : 2;  // normals (fused into the strip kernel)
+        if (!fuse_normals()) k += grid ? 1 : 2;  // normals (else fused into the strip kernel)
         return k;
     }
 };
@@ -246,6 +259,8 @@ static void pass_normals(cs_engine *h) {
     if (h->fp64) {
         launch_csr_normals_f64(h->N, h->plane, h->nc, (const double *)h->state[h->cur], h->tris_g,
                                (double *)h->face, h->inc_off, h->inc_tri, (double *)h->normals, h->st);
+    } else if (h->grid && !h->fixed && h->strip && (h->flags & CS_FLAG_PAIRED)) {
+        launch_pair_normals(h->sp, (const float *)h->state[h->cur], (float *)h->normals, h->st);
     } else if (h->grid) {
         launch_grid_normals(h->sp, h->fixed, (const float *)h->state[h->cur], (float *)h->normals, h->st);
     } else {
@@ -259,7 +274,7 @@ static void pass_normals(cs_engine *h) {
 // frame t runs inside frame t+1's force pass; the buffer is marked stale and
 // refreshed by a stand-alone normals launch only when it is read.
 static void launch_frame(cs_engine *h) {
-    const bool fuse = h->grid && h->strip;
+    const bool fuse = h->fuse_normals();
     pass_force_integrate(h, fuse);
     if (h->has_obstacle) {
         pass_detect(h);
@@ -595,7 +610,7 @@ extern "C" int cs_step(cs_engine *h, int32_t frames) {
             // replay the parity bookkeeping of one frame
             if (h->substeps & 1) h->cur = 1 - start;
             h->forces_valid = true;
-            h->normals_stale = h->grid && h->strip;
+            h->normals_stale = h->fuse_normals();
         } else {
             launch_frame(h);
             CK(cudaGetLastError());

@@ -173,6 +173,8 @@ void launch_strip_step(const StepParams &p, bool fixed, bool normals, const floa
                        cudaStream_t st, bool packed = false);
 void launch_pair3_step(const StepParams &p, bool normals, const float *src, float *dst,
                        const uint32_t *pinbits, const float *ext, float *nrm, cudaStream_t st);
+void launch_pair_normals(const StepParams &p, const float *state, float *nrm, cudaStream_t st);
+int pair3_rows(const StepParams &p);
 void launch_grid_forces(const StepParams &p, const float *src, int32_t *forces, cudaStream_t st);
 void launch_grid_normals(const StepParams &p, bool exact, const float *state, float *nrm,
                          cudaStream_t st);

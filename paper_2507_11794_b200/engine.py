@@ -212,7 +212,8 @@ class Engine:
     def __init__(self, mesh, obstacle=None, params=None, device=None,
                  pair_budget: int = DEFAULT_PAIR_BUDGET, *, precision: str = "fast",
                  graph: bool = True, stream=None, cell_size: float | None = None,
-                 force_csr: bool = False, kernel: str = "pair", narrow: str = "warp"):
+                 force_csr: bool = False, kernel: str = "pair", narrow: str = "warp",
+                 normals: str = "auto"):
         if precision not in PRECISIONS:
             raise ValueError(f"precision must be one of {PRECISIONS}")
         self.mesh = mesh
@@ -289,6 +290,13 @@ class Engine:
                              "(paired-column f32x2 warp strips) or 'tile' (shared-memory tiles)")
         if kernel == "tile":
             flags |= N.FLAG_TILE_KERNEL
+        if normals not in ("auto", "fused", "split"):
+            raise ValueError("normals must be 'auto', 'fused' (inside the next frame's step "
+                             "kernel) or 'split' (a stand-alone normals kernel every frame)")
+        if normals == "split":
+            flags |= N.FLAG_SPLIT_NORMALS
+        if normals == "fused":
+            flags |= N.FLAG_FUSE_NORMALS
         if narrow not in ("warp", "thread"):
             raise ValueError("narrow must be 'warp' (warp per query) or 'thread'")
         if narrow == "thread":

@@ -21,7 +21,8 @@ t1 = time.time()
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 eng = P.Engine(sc.mesh, sc.obstacle, sc.params, pair_budget=10**13, stream=stream.cuda_stream,
-               kernel=os.environ.get("CS_KERNEL", "strip"))
+               kernel=os.environ.get("CS_KERNEL", "pair"),
+               normals=os.environ.get("CS_NORMALS", "auto"))
 t2 = time.time()
 print(f"{cfg}: scene {t1 - t0:.1f}s engine {t2 - t1:.1f}s nodes {sc.mesh.num_nodes}", flush=True)
 flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device="cuda")
