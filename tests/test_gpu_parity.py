@@ -150,6 +150,26 @@ def test_narrow_phase_mappings_and_cell_sizes_are_bit_identical(narrow, cell):
     assert eng.stats()["hit_counter"] == int(g["eng_hits"].sum())
 
 
+@pytest.mark.parametrize("shape", [(67, 130), (130, 67), (800, 96)])
+@pytest.mark.parametrize("variant", [dict(), dict(normals="split"), dict(normals="fused"),
+                                     dict(kernel="strip"), dict(kernel="tile"),
+                                     dict(force_csr=True), dict(precision="fixed")])
+def test_normals_of_a_crumpled_cloth(shape, variant):
+    """Every normals path on a non-planar state (a flat hanging sheet has one
+    face normal everywhere and would hide row/column mix-ups)."""
+    sc = P.build_scene(P.ScenarioConfig("hanging", shape, dt=0.004))
+    rng = np.random.default_rng(3)
+    pos = sc.mesh.positions + rng.normal(scale=0.3 / max(shape), size=sc.mesh.positions.shape)
+    pos[:, 2] += 0.05 * np.sin(7 * sc.mesh.positions[:, 0]) * np.cos(5 * sc.mesh.positions[:, 1])
+    eng = P.Engine(sc.mesh, params=sc.params, **variant)
+    eng.write_positions(pos.astype(np.float32))
+    for frames in (1, 3):
+        eng.step_frames(frames)
+        now = eng.read_positions().astype(np.float64)
+        want = O.vertex_normals(sc.mesh.num_nodes, sc.mesh.triangles, now)
+        np.testing.assert_allclose(eng.read_normals(), want, atol=2e-5)
+
+
 def test_graph_replay_equals_eager_launches():
     g, a = _run_golden("traj_drop10.npz", "fixed")
     _, b = _run_golden("traj_drop10.npz", "fixed", graph=False)
