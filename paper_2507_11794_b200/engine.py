@@ -292,11 +292,8 @@ class Engine:
             flags |= N.FLAG_TILE_KERNEL
         if normals not in ("auto", "fused", "split"):
             raise ValueError("normals must be 'auto', 'fused' (inside the next frame's step "
-                             "kernel) or 'split' (a stand-alone normals kernel every frame)")
-        if normals == "split":
-            flags |= N.FLAG_SPLIT_NORMALS
-        if normals == "fused":
-            flags |= N.FLAG_FUSE_NORMALS
+                             "kernel) or 'split' (stand-alone kernel after each step)")
+        flags |= {"auto": 0, "split": N.FLAG_SPLIT_NORMALS, "fused": N.FLAG_FUSE_NORMALS}[normals]
         if narrow not in ("warp", "thread"):
             raise ValueError("narrow must be 'warp' (warp per query) or 'thread'")
         if narrow == "thread":

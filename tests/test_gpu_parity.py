@@ -152,6 +152,7 @@ def test_narrow_phase_mappings_and_cell_sizes_are_bit_identical(narrow, cell):
 
 @pytest.mark.parametrize("shape", [(67, 130), (130, 67), (800, 96)])
 @pytest.mark.parametrize("variant", [dict(), dict(normals="split"), dict(normals="fused"),
+                                     dict(normals="split", graph=False),
                                      dict(kernel="strip"), dict(kernel="tile"),
                                      dict(force_csr=True), dict(precision="fixed")])
 def test_normals_of_a_crumpled_cloth(shape, variant):
