@@ -161,6 +161,11 @@ int cs_destroy(cs_engine *h);
 /* Advance `frames` whole frames (asynchronous on the engine's stream). */
 int cs_step(cs_engine *h, int32_t frames);
 int cs_run_pass(cs_engine *h, int32_t pass_id);
+/* Advance `frames` frames, streaming every frame's positions ((N,3) f32) into
+   host_out[frames][N][3]: `step(readback=True)` (engine.py:341-343) for a
+   whole run, with each frame's device->host copy overlapping the next
+   frame's computation.  host_out should be page-locked. */
+int cs_record(cs_engine *h, int32_t frames, float *host_out);
 /* Respond pass alone; writes the responded count (synchronises). */
 int cs_respond(cs_engine *h, int64_t *responded);
 /* Synchronise and report the last frame's hit / respond counts. */

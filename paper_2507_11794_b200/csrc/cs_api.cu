@@ -107,6 +107,10 @@ struct cs_engine {
     void *stage = nullptr;
     size_t stage_bytes = 0;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    // cs_record: copy stream, per-parity events and device staging
+    cudaStream_t copy_st = nullptr;
+    cudaEvent_t ev_frame[2] = {nullptr, nullptr}, ev_moved[2] = {nullptr, nullptr};
+    float *rec_stage[2] = {nullptr, nullptr};
     int64_t frames = 0;
     StepParams sp{};
     CsrParams cp{};
@@ -561,6 +565,15 @@ extern "C" int cs_destroy(cs_engine *h) {
         if (p) cudaFree(p);
     if (h->has_obstacle) free_broadphase(h->bp);
     if (h->own_stream && h->st) cudaStreamDestroy(h->st);
+    if (h->copy_st) {
+        cudaStreamSynchronize(h->copy_st);
+        cudaStreamDestroy(h->copy_st);
+    }
+    for (int i = 0; i < 2; ++i) {
+        if (h->ev_frame[i]) cudaEventDestroy(h->ev_frame[i]);
+        if (h->ev_moved[i]) cudaEventDestroy(h->ev_moved[i]);
+        if (h->rec_stage[i]) cudaFree(h->rec_stage[i]);
+    }
     delete h;
     return 0;
 }
@@ -620,6 +633,42 @@ extern "C" int cs_step(cs_engine *h, int32_t frames) {
         }
         h->frames++;
     }
+    return 0;
+}
+
+// Advance `frames` frames and stream every frame's positions, (N,3) f32
+// each, into host_out[frames][N][3] -- engine.py:341-343 (`readback=True`)
+// for a whole run.  The device->host copy of frame f (a transpose kernel on a
+// copy stream, then the DMA) overlaps the computation of frame f+1; the
+// compute stream only waits for frame f's transpose (microseconds) before
+// reusing its buffer.  host_out should be pinned for the DMA to be async.
+extern "C" int cs_record(cs_engine *h, int32_t frames, float *host_out) {
+    if (!h || !host_out) return fail(CS_E_INVALID, "null argument");
+    if (h->fp64) return fail(CS_E_INVALID, "cs_record streams float32 positions");
+    if (!h->copy_st) {
+        CK(cudaStreamCreateWithFlags(&h->copy_st, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            CK(cudaEventCreateWithFlags(&h->ev_frame[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&h->ev_moved[i], cudaEventDisableTiming));
+            CK(cudaMalloc(&h->rec_stage[i], (size_t)h->N * 3 * sizeof(float)));
+        }
+    }
+    const int64_t nxx = h->grid ? h->nx : h->N;
+    for (int32_t f = 0; f < frames; ++f) {
+        const int k = f & 1;
+        if (f > 0) CK(cudaStreamWaitEvent(h->st, h->ev_moved[k ^ 1], 0));  // f-1 transposed
+        if (int r = cs_step(h, 1)) return r;
+        CK(cudaEventRecord(h->ev_frame[k], h->st));
+        CK(cudaStreamWaitEvent(h->copy_st, h->ev_frame[k], 0));
+        k_planes_to_aos<float><<<nb(h->N), 256, 0, h->copy_st>>>(
+            h->N, nxx, h->pitch, h->plane, 3, (const float *)h->state[h->cur], h->rec_stage[k]);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(h->ev_moved[k], h->copy_st));
+        CK(cudaMemcpyAsync(host_out + (size_t)f * h->N * 3, h->rec_stage[k],
+                           (size_t)h->N * 3 * sizeof(float), cudaMemcpyDeviceToHost, h->copy_st));
+    }
+    CK(cudaStreamSynchronize(h->copy_st));
+    CK(cudaStreamSynchronize(h->st));
     return 0;
 }
 

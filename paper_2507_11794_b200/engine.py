@@ -206,6 +206,19 @@ def _p(a):
     return None if a is None else a.ctypes.data
 
 
+def pinned_empty(shape, dtype=np.float32) -> np.ndarray:
+    """Page-locked host array (through torch's pinned allocator when torch is
+    importable, else an ordinary numpy array)."""
+    try:
+        import torch
+
+        tdt = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64,
+               np.dtype(np.int32): torch.int32}[np.dtype(dtype)]
+        return torch.empty(tuple(shape), dtype=tdt, pin_memory=True).numpy()
+    except Exception:
+        return np.empty(shape, dtype=dtype)
+
+
 class Engine:
     """A built B200 pipeline bound to one cloth/obstacle/params configuration."""
 
@@ -420,6 +433,22 @@ class Engine:
         """Advance `frames` frames with one call (graph replays, no sync)."""
         N.check(self._lib.cs_step(self._handle, int(frames)))
         self.frame_count += int(frames)
+
+    def simulate(self, frames: int, out=None) -> np.ndarray:
+        """Advance `frames` frames and return every frame's positions as a
+        (frames, N, 3) float32 array -- `step(readback=True)` for a whole run
+        (engine.py:341-343), with frame f's device->host copy overlapping the
+        computation of frame f+1.  `out` should be page-locked
+        (`pinned_empty`); a pageable array works but copies synchronously."""
+        frames = int(frames)
+        if out is None:
+            out = pinned_empty((frames, self.num_nodes, 3))
+        if out.shape != (frames, self.num_nodes, 3) or out.dtype != np.float32 \
+                or not out.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous float32 array of shape (frames, N, 3)")
+        N.check(self._lib.cs_record(self._handle, frames, out.ctypes.data))
+        self.frame_count += frames
+        return out
 
     def run_respond_pass(self) -> int:
         """Respond kernel alone (engine.py:346-352); returns nodes moved."""

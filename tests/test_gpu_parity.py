@@ -171,6 +171,23 @@ def test_normals_of_a_crumpled_cloth(shape, variant):
         np.testing.assert_allclose(eng.read_normals(), want, atol=2e-5)
 
 
+@pytest.mark.parametrize("substeps", [1, 2])
+def test_simulate_streams_every_frame(substeps):
+    """Engine.simulate (cs_record) returns exactly what step()+read_positions()
+    returns frame by frame, copies overlapping the next frame."""
+    sc = P.build_scene(P.ScenarioConfig("hanging", (61, 47), dt=0.004))
+    params = P.SimParams(dt=sc.params.dt, stiffness=sc.params.stiffness,
+                         damping=sc.params.damping, substeps=substeps)
+    a = P.Engine(sc.mesh, params=params)
+    b = P.Engine(sc.mesh, params=params)
+    traj = a.simulate(9)
+    for f in range(9):
+        b.step()
+        np.testing.assert_array_equal(traj[f], b.read_positions())
+    assert a.frame_count == 9
+    np.testing.assert_array_equal(a.read_velocities(), b.read_velocities())
+
+
 def test_graph_replay_equals_eager_launches():
     g, a = _run_golden("traj_drop10.npz", "fixed")
     _, b = _run_golden("traj_drop10.npz", "fixed", graph=False)
