@@ -166,6 +166,12 @@ int cs_run_pass(cs_engine *h, int32_t pass_id);
    whole run, with each frame's device->host copy overlapping the next
    frame's computation.  host_out should be page-locked. */
 int cs_record(cs_engine *h, int32_t frames, float *host_out);
+/* Contact log for parity checks: record every (cloth node, obstacle
+   triangle) contact of subsequent detect passes (collision.py:218-240
+   Contact.nodes per hit); capacity 0 turns it off.  cs_read_contacts returns
+   the last frame's pairs (node index, triangle) and their total count. */
+int cs_contact_log(cs_engine *h, int64_t capacity);
+int cs_read_contacts(cs_engine *h, int32_t *out, int64_t max, int64_t *n);
 /* Respond pass alone; writes the responded count (synchronises). */
 int cs_respond(cs_engine *h, int64_t *responded);
 /* Synchronise and report the last frame's hit / respond counts. */

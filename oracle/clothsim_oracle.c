@@ -214,17 +214,36 @@ static void sol_offset(const double *p, const double *hit, const double *fn, dou
     out[0] = nx * scale; out[1] = ny * scale; out[2] = nz * scale;
 }
 
-typedef struct { i64 node; double off[3]; } sol_contact;
+typedef struct { i64 node, tri; double off[3]; } sol_contact;
 typedef struct { sol_contact *v; i64 n, cap; i64 hits; } sol_list;
 
-static void list_push(sol_list *l, i64 node, const double *off) {
+static void list_push(sol_list *l, i64 node, i64 tri, const double *off) {
     if (l->n == l->cap) {
         l->cap = l->cap ? 2 * l->cap : 64;
         l->v = (sol_contact *)realloc(l->v, sizeof(sol_contact) * l->cap);
     }
     l->v[l->n].node = node;
+    l->v[l->n].tri = tri;
     memcpy(l->v[l->n].off, off, sizeof(double) * 3);
     l->n++;
+}
+
+/* optional (node, obstacle triangle) log of the contacts of or_sol_detect,
+ * in the solver's order (collision.py:218-240 Contact.nodes per hit) */
+static i32 *g_clog = NULL;
+static i64 g_clog_cap = 0, g_clog_n = 0;
+OR_EXPORT void or_sol_contact_log(i32 *buf, i64 cap) {
+    g_clog = buf;
+    g_clog_cap = cap;
+    g_clog_n = 0;
+}
+OR_EXPORT i64 or_sol_contact_count(void) { return g_clog_n; }
+static void clog_push(i64 node, i64 tri) {
+    if (g_clog && g_clog_n < g_clog_cap) {
+        g_clog[2 * g_clog_n] = (i32)node;
+        g_clog[2 * g_clog_n + 1] = (i32)tri;
+    }
+    g_clog_n++;
 }
 
 /* collision.detect_all (collision.py:243-315): every unique cloth edge vs
@@ -238,6 +257,7 @@ OR_EXPORT i64 or_sol_detect(i64 n, const double *pos, i64 ne, const i32 *edges, 
                             i64 *count) {
     int nth = g_threads;
     i64 hits = 0;
+    g_clog_n = 0;
     for (i64 i = 0; i < 3 * n; ++i) acc[i] = 0.0;
     for (i64 i = 0; i < n; ++i) count[i] = 0;
     /* pass A: cloth edges vs obstacle triangles */
@@ -263,9 +283,9 @@ OR_EXPORT i64 or_sol_detect(i64 n, const double *pos, i64 ne, const i32 *edges, 
                     double off[3];
                     L->hits++;
                     sol_offset(pa, hit, fn, sign, margin, off);
-                    list_push(L, edges[2 * e], off);
+                    list_push(L, edges[2 * e], t, off);
                     sol_offset(pb, hit, fn, sign, margin, off);
-                    list_push(L, edges[2 * e + 1], off);
+                    list_push(L, edges[2 * e + 1], t, off);
                 }
             }
         }
@@ -275,6 +295,7 @@ OR_EXPORT i64 or_sol_detect(i64 n, const double *pos, i64 ne, const i32 *edges, 
                 i64 nd = L->v[q].node;
                 for (int d = 0; d < 3; ++d) acc[3 * nd + d] += L->v[q].off[d];
                 count[nd] += 1;
+                clog_push(nd, L->v[q].tri);
             }
             hits += L->hits;
             free(L->v);
@@ -310,11 +331,11 @@ OR_EXPORT i64 or_sol_detect(i64 n, const double *pos, i64 ne, const i32 *edges, 
                         double off[3];
                         L->hits++;
                         sol_offset(c0, hit, fn, sign, margin, off);
-                        list_push(L, ct[0], off);
+                        list_push(L, ct[0], t, off);
                         sol_offset(c1, hit, fn, sign, margin, off);
-                        list_push(L, ct[1], off);
+                        list_push(L, ct[1], t, off);
                         sol_offset(c2, hit, fn, sign, margin, off);
-                        list_push(L, ct[2], off);
+                        list_push(L, ct[2], t, off);
                     }
                 }
             }
@@ -325,6 +346,7 @@ OR_EXPORT i64 or_sol_detect(i64 n, const double *pos, i64 ne, const i32 *edges, 
                 i64 nd = L->v[q].node;
                 for (int d = 0; d < 3; ++d) acc[3 * nd + d] += L->v[q].off[d];
                 count[nd] += 1;
+                clog_push(nd, L->v[q].tri);
             }
             hits += L->hits;
             free(L->v);

@@ -60,6 +60,8 @@ def lib():
             "or_sol_integrate": (I, [I, P, P, P, P, P, P, D, C]),
             "or_sol_detect": (I, [I, P, I, P, I, P, I, P, P, P, D, D, P, P]),
             "or_sol_respond": (I, [I, P, P, P, P, P, C]),
+            "or_sol_contact_log": (None, [P, I]),
+            "or_sol_contact_count": (I, []),
             "or_sol_face_normals": (None, [I, P, P, P]),
             "or_sol_vertex_normals": (None, [I, I, P, P, P]),
             "or_encode": (ctypes.c_int32, [F, F]),
@@ -237,6 +239,22 @@ class SolverOracle:
             float(self.params.epsilon_mt), float(self.params.response_margin), _p(acc), _p(cnt))
         return acc, cnt, int(hits)
 
+    def detect_contacts(self, capacity=1 << 22):
+        """detect_all at the current positions, returning (hits, contacts):
+        contacts is an (n, 2) int32 array of (cloth node, obstacle triangle)
+        in the solver's order (collision.py:243-315, Contact.nodes)."""
+        buf = np.zeros((capacity, 2), dtype=np.int32)
+        L = lib()
+        L.or_sol_contact_log(_p(buf), capacity)
+        try:
+            _, _, hits = self.detect()
+            n = int(L.or_sol_contact_count())
+        finally:
+            L.or_sol_contact_log(None, 0)
+        if n > capacity:
+            raise RuntimeError("contact log truncated")
+        return hits, buf[:n].copy()
+
     def step(self, normals=True) -> int:
         L = lib()
         p = self.params
@@ -353,6 +371,33 @@ class EngineOracle:
         self.update_normals()
         self.frame_count += 1
         return hits, responded
+
+
+def boundary_distance(start, end, v0, v1, v2, eps=1e-6):
+    """Distance of the segment-triangle decision quantities to the nearest
+    predicate boundary, in float64 -- used to classify contacts on which a
+    float32 and a float64 evaluation may legitimately disagree.  Restates
+    the reference test oracle's classifier (pkg/tests/oracles.py:81-116):
+    |a| vs eps, u vs 0/1, v vs 0, u+v vs 1, t vs eps and |d|."""
+    s, e = np.asarray(start, np.float64), np.asarray(end, np.float64)
+    v0, v1, v2 = (np.asarray(x, np.float64) for x in (v0, v1, v2))
+    d = e - s
+    dl = float(np.linalg.norm(d))
+    if dl == 0.0:
+        return 0.0
+    r = d / dl
+    e1, e2 = v1 - v0, v2 - v0
+    h = np.cross(r, e2)
+    a = float(e1 @ h)
+    m = [abs(abs(a) - eps)]
+    if abs(a) >= eps:
+        f = 1.0 / a
+        q = np.cross(s - v0, e1)
+        u = f * float((s - v0) @ h)
+        v = f * float(r @ q)
+        t = f * float(e2 @ q)
+        m += [abs(u), abs(1.0 - u), abs(v), abs(u + v - 1.0), abs(t - eps), abs(dl - t)]
+    return min(m)
 
 
 def encode(x, scale=1 << 16):

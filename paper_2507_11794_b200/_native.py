@@ -91,6 +91,8 @@ SIGNATURES = {
     "cs_step": (_I32, [_P, _I32]),
     "cs_run_pass": (_I32, [_P, _I32]),
     "cs_record": (_I32, [_P, _I32, _P]),
+    "cs_contact_log": (_I32, [_P, _I64]),
+    "cs_read_contacts": (_I32, [_P, _P, _I64, ctypes.POINTER(_I64)]),
     "cs_respond": (_I32, [_P, ctypes.POINTER(_I64)]),
     "cs_frame_stats": (_I32, [_P, ctypes.POINTER(CsStats)]),
     "cs_frame_hits": (_I32, [_P, _I64, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),

@@ -107,6 +107,9 @@ struct cs_engine {
     void *stage = nullptr;
     size_t stage_bytes = 0;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    // optional contact log (cs_contact_log / cs_read_contacts)
+    uint32_t *clog = nullptr, *clog_n = nullptr;
+    int64_t clog_cap = 0;
     // cs_record: copy stream, per-parity events and device staging
     cudaStream_t copy_st = nullptr;
     cudaEvent_t ev_frame[2] = {nullptr, nullptr}, ev_moved[2] = {nullptr, nullptr};
@@ -130,6 +133,9 @@ struct cs_engine {
         A.frame_counter = stats + 3;
         A.ring = stats + 4;
         A.ring_size = kRing;
+        A.clog = clog;
+        A.clog_n = clog_n;
+        A.clog_cap = (uint32_t)clog_cap;
         A.eps = eps;
         A.margin = margin;
         A.pad = 1e-5f;  // kernels.py:48 BOX_PAD
@@ -247,6 +253,7 @@ static void pass_force_integrate(cs_engine *h, bool fuse_normals = false) {
 
 static void pass_detect(cs_engine *h) {
     cudaMemsetAsync(h->stats, 0, 2 * sizeof(unsigned long long), h->st);
+    if (h->clog) cudaMemsetAsync(h->clog_n, 0, sizeof(uint32_t), h->st);
     if (!h->has_obstacle) return;
     launch_detect(h->cargs(), h->bp, h->corners, h->onormals, h->edges_g, h->ne, h->tris_g, h->nc,
                   h->st);
@@ -569,6 +576,8 @@ extern "C" int cs_destroy(cs_engine *h) {
         cudaStreamSynchronize(h->copy_st);
         cudaStreamDestroy(h->copy_st);
     }
+    if (h->clog) cudaFree(h->clog);
+    if (h->clog_n) cudaFree(h->clog_n);
     for (int i = 0; i < 2; ++i) {
         if (h->ev_frame[i]) cudaEventDestroy(h->ev_frame[i]);
         if (h->ev_moved[i]) cudaEventDestroy(h->ev_moved[i]);
@@ -669,6 +678,48 @@ extern "C" int cs_record(cs_engine *h, int32_t frames, float *host_out) {
     }
     CK(cudaStreamSynchronize(h->copy_st));
     CK(cudaStreamSynchronize(h->st));
+    return 0;
+}
+
+// Record every (cloth node, obstacle triangle) contact of the following
+// detect passes (capacity 0 switches the log off).
+extern "C" int cs_contact_log(cs_engine *h, int64_t capacity) {
+    if (!h || capacity < 0) return fail(CS_E_INVALID, "bad argument");
+    CK(cudaStreamSynchronize(h->st));
+    if (h->clog) cudaFree(h->clog);
+    if (h->clog_n) cudaFree(h->clog_n);
+    h->clog = nullptr;
+    h->clog_n = nullptr;
+    h->clog_cap = 0;
+    if (capacity > 0) {
+        CK(dalloc(&h->clog, 2 * capacity));
+        CK(dalloc(&h->clog_n, 1));
+        CK(cudaMemset(h->clog_n, 0, sizeof(uint32_t)));
+        h->clog_cap = capacity;
+    }
+    drop_graphs(h);  // the detect kernels' arguments changed
+    return 0;
+}
+
+// The last frame's contacts as (node index, triangle) int32 pairs; *n gets
+// the total count (which may exceed `max` -- then the log was truncated).
+extern "C" int cs_read_contacts(cs_engine *h, int32_t *out, int64_t max, int64_t *n) {
+    if (!h || !n) return fail(CS_E_INVALID, "null argument");
+    if (!h->clog) return fail(CS_E_INVALID, "contact log is off (cs_contact_log)");
+    uint32_t cnt = 0;
+    CK(cudaMemcpyAsync(&cnt, h->clog_n, sizeof(cnt), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    *n = cnt;
+    const int64_t k = std::min<int64_t>(std::min<int64_t>(cnt, h->clog_cap), max);
+    if (k > 0 && out) {
+        std::vector<uint32_t> raw(2 * k);
+        CK(cudaMemcpy(raw.data(), h->clog, 2 * k * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < k; ++i) {
+            const int64_t g = raw[2 * i];
+            out[2 * i] = (int32_t)(h->grid ? (g / h->pitch) * h->nx + g % h->pitch : g);
+            out[2 * i + 1] = (int32_t)raw[2 * i + 1];
+        }
+    }
     return 0;
 }
 

@@ -385,7 +385,14 @@ __device__ __forceinline__ float np_max(float a, float b) {
 // _accumulate_hits (kernels.py:171-183) for one node; returns true when the
 // node's count went 0 -> 1 (it joins the touched list).
 __device__ __forceinline__ void accumulate(const CollideArgs &A, int64_t g, const float *p,
-                                           const float *hit, const float *on) {
+                                           const float *hit, const float *on, uint32_t tri) {
+    if (A.clog) {  // optional (node, triangle) contact log for the parity tests
+        const uint32_t slot = atomicAdd(A.clog_n, 1u);
+        if (slot < A.clog_cap) {
+            A.clog[2 * slot] = (uint32_t)g;
+            A.clog[2 * slot + 1] = tri;
+        }
+    }
     const float depth0 = -dot3x(fsub(p[0], hit[0]), fsub(p[1], hit[1]), fsub(p[2], hit[2]), on[0],
                                 on[1], on[2]);
     const float depth = np_max(depth0, 0.f);
@@ -468,8 +475,8 @@ k_detect_cloth_edges(const CollideArgs A, const GridDesc g, const uint32_t *__re
                             const float sign = np_max(sa, sb) >= 0.f ? 1.f : -1.f;
                             const float on[3] = {fmul(nrm[0], sign), fmul(nrm[1], sign),
                                                  fmul(nrm[2], sign)};
-                            accumulate(A, ga, st, pt, on);
-                            accumulate(A, gb, en, pt, on);
+                            accumulate(A, ga, st, pt, on, t);
+                            accumulate(A, gb, en, pt, on, t);
                         }
                     }
         }
@@ -545,9 +552,9 @@ k_detect_obstacle_edges(const CollideArgs A, const GridDesc g, const uint32_t *_
                                 const float sign = total >= 0.f ? 1.f : -1.f;
                                 const float on[3] = {fmul(nrm[0], sign), fmul(nrm[1], sign),
                                                      fmul(nrm[2], sign)};
-                                accumulate(A, n0, v0, pt, on);
-                                accumulate(A, n1, v1, pt, on);
-                                accumulate(A, n2, v2, pt, on);
+                                accumulate(A, n0, v0, pt, on, t);
+                                accumulate(A, n1, v1, pt, on, t);
+                                accumulate(A, n2, v2, pt, on, t);
                             }
                         }
                     }
@@ -710,8 +717,8 @@ k_detect_warp(const CollideArgs A, const GridDesc g, const uint32_t *__restrict_
                                                fsub(v[1][2], pt[2]), nrm[0], nrm[1], nrm[2]);
                         const float sign = np_max(sa, sb) >= 0.f ? 1.f : -1.f;
                         const float on[3] = {fmul(nrm[0], sign), fmul(nrm[1], sign), fmul(nrm[2], sign)};
-                        accumulate(A, nid[0], v[0], pt, on);
-                        accumulate(A, nid[1], v[1], pt, on);
+                        accumulate(A, nid[0], v[0], pt, on, tri);
+                        accumulate(A, nid[1], v[1], pt, on, tri);
                     } else {
                         for (int slot = 0; slot < 3; ++slot) {
                             const float *st = cr + 3 * slot;
@@ -734,9 +741,9 @@ k_detect_warp(const CollideArgs A, const GridDesc g, const uint32_t *__restrict_
                                                     fsub(v[2][2], pt[2]), nrm[0], nrm[1], nrm[2]);
                             const float sign = fadd(fadd(t0s, t1s), t2s) >= 0.f ? 1.f : -1.f;
                             const float on[3] = {fmul(nrm[0], sign), fmul(nrm[1], sign), fmul(nrm[2], sign)};
-                            accumulate(A, nid[0], v[0], pt, on);
-                            accumulate(A, nid[1], v[1], pt, on);
-                            accumulate(A, nid[2], v[2], pt, on);
+                            accumulate(A, nid[0], v[0], pt, on, tri);
+                            accumulate(A, nid[1], v[1], pt, on, tri);
+                            accumulate(A, nid[2], v[2], pt, on, tri);
                         }
                     }
                 }

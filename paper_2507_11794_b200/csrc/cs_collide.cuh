@@ -67,6 +67,9 @@ struct CollideArgs {
     unsigned long long *frame_counter;
     unsigned long long *ring;         // per-frame (hits, responded), ring_size frames
     int ring_size;
+    uint32_t *clog;                   // optional contact log: (storage node, triangle)
+    uint32_t *clog_n;
+    uint32_t clog_cap;
     float eps, margin, pad, scale_f;
     double scale_d;
 };

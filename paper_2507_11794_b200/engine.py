@@ -450,6 +450,23 @@ class Engine:
         self.frame_count += frames
         return out
 
+    def enable_contact_log(self, capacity: int = 1 << 22) -> None:
+        """Record every (cloth node, obstacle triangle) contact of later
+        frames (parity checks); capacity 0 switches it off."""
+        N.check(self._lib.cs_contact_log(self._handle, int(capacity)))
+        self._clog_cap = int(capacity)
+
+    def read_contacts(self) -> np.ndarray:
+        """The last frame's contacts as an (n, 2) int32 array of (node,
+        triangle), one row per pushed node per hit (duplicates kept)."""
+        cap = getattr(self, "_clog_cap", 0)
+        out = np.empty((max(cap, 1), 2), dtype=np.int32)
+        n = ctypes.c_int64()
+        N.check(self._lib.cs_read_contacts(self._handle, out.ctypes.data, cap, ctypes.byref(n)))
+        if n.value > cap:
+            raise RuntimeError(f"contact log truncated: {n.value} contacts, capacity {cap}")
+        return out[: n.value].copy()
+
     def run_respond_pass(self) -> int:
         """Respond kernel alone (engine.py:346-352); returns nodes moved."""
         r = ctypes.c_int64()

@@ -48,6 +48,50 @@ def test_banded_run_is_bit_identical_to_one_engine(world, precision):
     np.testing.assert_array_equal(got, whole.read_positions())
 
 
+@pytest.mark.parametrize("spec", [("icosphere:2", (24, 24), 120), ("uvsphere:40x40", (64, 64), 90)])
+def test_contact_set_matches_f64_solver_except_boundary_pairs(spec):
+    """North-star contact gate: the (node, triangle) contact set of a GPU
+    detect pass equals the float64 reference solver's (detect_all,
+    collision.py:243-315) at the same positions, except pairs whose
+    predicate quantities lie within 1e-5 of a decision boundary."""
+    from collections import Counter
+
+    from oracle import oracle as O
+    from paper_2507_11794_b200 import _native as N
+
+    obstacle, grid, frames = spec
+    sc = P.build_scene(P.ScenarioConfig("drop", grid, obstacle=obstacle))
+    eng = P.Engine(sc.mesh, sc.obstacle, sc.params, pair_budget=10**13)
+    eng.step_frames(frames)
+    eng.enable_contact_log(1 << 20)
+    N.check(eng._lib.cs_run_pass(eng._handle, N.PASS_FORCE_INTEGRATE))
+    pos = eng.read_positions()
+    N.check(eng._lib.cs_run_pass(eng._handle, N.PASS_DETECT))
+    gpu = Counter(map(tuple, eng.read_contacts().tolist()))
+    so = O.SolverOracle(sc.mesh, sc.params, sc.obstacle)
+    so.pos[...] = pos.astype(np.float64)
+    O.set_threads(O.max_threads())
+    hits, ref_arr = so.detect_contacts()
+    ref = Counter(map(tuple, ref_arr.tolist()))
+    assert hits > 0 and sum(ref.values()) > 0
+    diff = (gpu - ref) + (ref - gpu)
+    tris = np.asarray(sc.mesh.triangles)
+    ov, ot = sc.obstacle.vertices, sc.obstacle.triangles
+    p64 = pos.astype(np.float64)
+    for node, t in diff:
+        cand = []
+        for c in np.nonzero((tris == node).any(axis=1))[0]:
+            a, b, d = tris[c]
+            for u, w in ((a, b), (b, d), (d, a)):  # cloth edges through the node
+                if node in (u, w):
+                    cand.append(O.boundary_distance(p64[u], p64[w], *ov[ot[t]]))
+            for s in range(3):  # obstacle edges of t vs this cloth triangle
+                cand.append(O.boundary_distance(ov[ot[t][s]], ov[ot[t][(s + 1) % 3]],
+                                                p64[a], p64[b], p64[d]))
+        assert min(cand) < 1e-5, (node, t, min(cand))
+    assert sum(diff.values()) <= max(4, 0.01 * sum(ref.values()))
+
+
 def test_c3_drapes_finite_with_contacts_in_both_modes():
     sc = P.baseline_scene("C3")
     hits = {}
