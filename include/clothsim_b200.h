@@ -189,6 +189,39 @@ int cs_synchronize(cs_engine *h);
    which = 0..5 -> x, y, z, vx, vy, vz of the CURRENT state; returns the
    pitch (elements per grid row) through *pitch. */
 int cs_state_plane(cs_engine *h, int32_t which, void **dev_ptr, int64_t *pitch);
+/* ---- row bands (BASELINE config 5; no reference counterpart -- the
+   reference runs one WebGPU device) ----
+   One engine per GPU holds owned rows [row_lo, row_hi) of its local sheet
+   plus a 2-row halo each side (bend springs reach two rows, mesh.py:284-289;
+   damping reads neighbour velocities, solver.py:117-119).  A neighbour is
+   described by its two state buffers and flag words (cs_state_buffers; across
+   processes through cs_ipc_export / cs_ipc_open), and the step kernel stores
+   my rows [src_row0, src_row0+rows) straight into its rows
+   [dst_row0, dst_row0+rows) -- the halo exchange happens inside the step, as
+   peer stores over NVLink -- then signals `remote_flag` (the neighbour's flag
+   word 0 if I am its upper neighbour, 1 if its lower one).  Before each force
+   pass an engine's stream waits until every neighbour finished the previous
+   pass.  Link before the first frame; every band must step in lockstep. */
+typedef struct cs_halo_peer {
+    void *state[2];        /* the neighbour's state buffers (cs_state_buffers) */
+    int64_t plane;         /* the neighbour's plane stride in elements */
+    int64_t src_row0;      /* first of MY local rows sent to it */
+    int64_t dst_row0;      /* where that row lands in ITS local rows */
+    int64_t rows;          /* rows sent (the halo depth) */
+    uint32_t *remote_flag; /* its flag word for me */
+} cs_halo_peer;
+/* The two ping-pong state buffers (6 planes each), the two flag words
+   ([0] written by the upper neighbour, [1] by the lower), plane stride and
+   pitch in elements. */
+int cs_state_buffers(cs_engine *h, void **state0, void **state1, uint32_t **flags,
+                     int64_t *plane, int64_t *pitch);
+int cs_set_halo_peers(cs_engine *h, int64_t row_lo, int64_t row_hi, const cs_halo_peer *up,
+                      const cs_halo_peer *down);
+/* cudaIpcGetMemHandle / cudaIpcOpenMemHandle of an engine allocation
+   (a state buffer or the flag words), as 64 opaque bytes. */
+int cs_ipc_export(void *dev_ptr, uint8_t handle[64]);
+int cs_ipc_open(const uint8_t handle[64], void **dev_ptr);
+int cs_ipc_close(void *dev_ptr);
 /* Number of kernels one cs_step(h, 1) launches. */
 int cs_kernels_per_frame(cs_engine *h, int32_t *count);
 /* Broad-phase statistics: cells, references, last frame's candidate pairs. */

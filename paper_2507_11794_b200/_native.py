@@ -84,6 +84,17 @@ class CsStats(ctypes.Structure):
     _fields_ = [("hits", _I64), ("responded", _I64), ("frames", _I64), ("hit_counter", _I64)]
 
 
+class CsHaloPeer(ctypes.Structure):
+    _fields_ = [
+        ("state", _P * 2),
+        ("plane", _I64),
+        ("src_row0", _I64),
+        ("dst_row0", _I64),
+        ("rows", _I64),
+        ("remote_flag", _P),
+    ]
+
+
 # every symbol include/clothsim_b200.h declares, with its signature
 SIGNATURES = {
     "cs_create": (_I32, [ctypes.POINTER(CsDesc), ctypes.POINTER(_P)]),
@@ -101,6 +112,13 @@ SIGNATURES = {
     "cs_inject_response": (_I32, [_P, _I64, ctypes.POINTER(_I32), _I32]),
     "cs_synchronize": (_I32, [_P]),
     "cs_state_plane": (_I32, [_P, _I32, ctypes.POINTER(_P), ctypes.POINTER(_I64)]),
+    "cs_state_buffers": (_I32, [_P, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_P),
+                                ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
+    "cs_set_halo_peers": (_I32, [_P, _I64, _I64, ctypes.POINTER(CsHaloPeer),
+                                 ctypes.POINTER(CsHaloPeer)]),
+    "cs_ipc_export": (_I32, [_P, ctypes.c_char_p]),
+    "cs_ipc_open": (_I32, [ctypes.c_char_p, ctypes.POINTER(_P)]),
+    "cs_ipc_close": (_I32, [_P]),
     "cs_kernels_per_frame": (_I32, [_P, ctypes.POINTER(_I32)]),
     "cs_broadphase_stats": (_I32, [_P, ctypes.POINTER(_I64)]),
     "cs_last_error": (ctypes.c_char_p, []),

@@ -11,15 +11,28 @@ finding 3).  Per frame:
      bottom halo, rows [j1-2, j1) to rank+1's top halo (torch.distributed
      point-to-point: NCCL over NVLink on GPUs, gloo on CPU tensors).
 
+Two exchange mechanisms:
+
+* ``exchange="p2p"`` (default on GPUs): step 2 disappears into step 1.  The
+  step kernel stores each boundary row straight into the neighbour's halo
+  (peer memory over NVLink; CUDA IPC handles are swapped once through
+  torch.distributed), and a stream-ordered handshake (cuStreamWaitValue32 /
+  cuStreamWriteValue32 on per-neighbour flag words) orders the passes -- no
+  NCCL call, no packing kernel, no host synchronisation per frame
+  (cs_set_halo_peers in include/clothsim_b200.h).
+* ``exchange="nccl"``: torch.distributed point-to-point after each step
+  (``exchange_halos``), the plain baseline; also what the CPU gloo tests run.
+
 Because each node's force sums the same springs in the same program order
 whatever band it sits in, a banded run is bit-identical to the single-GPU
-run (tests/test_bands_gloo.py checks the exchange on CPU; the GPU test steps
-several bands in one process).  The obstacle (if any) would be replicated per
-rank; collision across band seams is not implemented in this round.
+run (tests/test_bands_gloo.py checks the exchange plans on CPU; the GPU
+tests link several bands in one process).  The obstacle (if any) would be
+replicated per rank; collision across band seams is not implemented yet.
 """
 
 from __future__ import annotations
 
+import ctypes
 import json
 import os
 import time
@@ -57,6 +70,21 @@ class HaloPlan:
         self.recv_up = (0, self.j0 - self.l0)                                  # my top halo
         self.send_down = (self.j1 - self.l0 - halo, self.j1 - self.l0)         # my last owned rows
         self.recv_down = (self.j1 - self.l0, self.l1 - self.l0)                # my bottom halo
+
+
+def peer_rows(me: HaloPlan, nbr: HaloPlan, direction: str):
+    """(src_row0, dst_row0, rows): my local rows stored into neighbour `nbr`'s
+    halo -- `direction` "up" for rank-1 (my first owned rows -> its bottom
+    halo), "down" for rank+1 (my last owned rows -> its top halo)."""
+    if direction == "up":
+        src, dst = me.send_up, nbr.recv_down
+    elif direction == "down":
+        src, dst = me.send_down, nbr.recv_up
+    else:
+        raise ValueError(direction)
+    if src[1] - src[0] != dst[1] - dst[0]:
+        raise ValueError("halo plans of neighbouring bands disagree")
+    return src[0], dst[0], src[1] - src[0]
 
 
 def exchange_halos(planes, plan: HaloPlan, group=None):
@@ -112,10 +140,16 @@ class BandedEngine:
     in rows), stepped on this rank's GPU, halos exchanged over NCCL."""
 
     def __init__(self, nx, ny, params, rank, world, group=None, stream=None, width=1.0,
-                 height=1.0, node_mass=0.05, pinned_rows="first"):
+                 height=1.0, node_mass=0.05, pinned_rows="first", exchange="nccl",
+                 precision="fast", **engine_kw):
         from .engine import Engine
         from .mesh import grid_band
 
+        if exchange not in ("nccl", "p2p"):
+            raise ValueError("exchange must be 'nccl' or 'p2p'")
+        self.exchange = exchange
+        self.linked = False
+        self._opened = []
         self.plan = HaloPlan(ny, world, rank)
         self.nx, self.ny = nx, ny
         mesh = grid_band(nx, ny, self.plan.l0, self.plan.l1, width, height,
@@ -125,9 +159,94 @@ class BandedEngine:
         rot[:, 1] = -mesh.positions[:, 2]
         mesh.positions = rot
         self.mesh = mesh
-        self.engine = Engine(mesh, params=params, stream=stream)
+        self.engine = Engine(mesh, params=params, stream=stream, precision=precision, **engine_kw)
         self.group = group
         self.local_rows = self.plan.l1 - self.plan.l0
+
+    # ---- p2p linking ---------------------------------------------------------
+    def buffers(self):
+        """Device pointers of this band's state buffers and flag words."""
+        from . import _native as N
+
+        s0, s1, fl = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        plane, pitch = ctypes.c_int64(), ctypes.c_int64()
+        N.check(self.engine._lib.cs_state_buffers(self.engine._handle, ctypes.byref(s0),
+                                                  ctypes.byref(s1), ctypes.byref(fl),
+                                                  ctypes.byref(plane), ctypes.byref(pitch)))
+        return {"state": (s0.value, s1.value), "flags": fl.value, "plane": plane.value,
+                "pitch": pitch.value}
+
+    def link(self, up=None, down=None):
+        """Make the step kernel store boundary rows into the neighbours.
+
+        `up` / `down` are ``(buffers_dict, HaloPlan)`` of rank-1 / rank+1 with
+        pointers valid in this process (same device, or opened IPC handles)."""
+        from . import _native as N
+
+        def peer(nb, direction):
+            if nb is None:
+                return None
+            info, nplan = nb
+            src, dst, rows = peer_rows(self.plan, nplan, direction)
+            p = N.CsHaloPeer()
+            p.state[0], p.state[1] = info["state"]
+            p.plane, p.src_row0, p.dst_row0, p.rows = info["plane"], src, dst, rows
+            # the neighbour's flag word 1 is written by its lower neighbour
+            # (me, when it is above me), word 0 by its upper neighbour
+            p.remote_flag = info["flags"] + 4 * (1 if direction == "up" else 0)
+            return p
+
+        pu, pd = peer(up, "up"), peer(down, "down")
+        lo, hi = self.plan.j0 - self.plan.l0, self.plan.j1 - self.plan.l0
+        N.check(self.engine._lib.cs_set_halo_peers(
+            self.engine._handle, lo, hi, ctypes.byref(pu) if pu else None,
+            ctypes.byref(pd) if pd else None))
+        self.linked = True
+
+    def link_ipc(self):
+        """Multi-process linking: swap CUDA IPC handles of the state buffers and
+        flag words with the neighbouring ranks over torch.distributed."""
+        import torch.distributed as dist
+
+        from . import _native as N
+
+        lib = self.engine._lib
+        info = self.buffers()
+
+        def export(ptr):
+            buf = ctypes.create_string_buffer(64)
+            N.check(lib.cs_ipc_export(ptr, buf))
+            return buf.raw
+
+        mine = {"rank": self.plan.rank, "plane": info["plane"], "ny": self.plan.l1,
+                "h": [export(info["state"][0]), export(info["state"][1]), export(info["flags"])]}
+        allinfo = [None] * self.plan.world
+        dist.all_gather_object(allinfo, mine, group=self.group)
+
+        def open_nbr(r):
+            if r is None:
+                return None
+            ptrs = []
+            for hbytes in allinfo[r]["h"]:
+                p = ctypes.c_void_p()
+                N.check(lib.cs_ipc_open(hbytes, ctypes.byref(p)))
+                self._opened.append(p.value)
+                ptrs.append(p.value)
+            nplan = HaloPlan(self.ny, self.plan.world, r)
+            return ({"state": (ptrs[0], ptrs[1]), "flags": ptrs[2],
+                     "plane": allinfo[r]["plane"]}, nplan)
+
+        self.link(open_nbr(self.plan.up), open_nbr(self.plan.down))
+        dist.barrier(group=self.group)  # every band linked before anyone steps
+
+    def close(self):
+        from . import _native as N
+
+        self.engine.synchronize()
+        for p in self._opened:
+            N.check(self.engine._lib.cs_ipc_close(p))
+        self._opened = []
+        self.engine.close()
 
     def planes(self):
         import torch
@@ -138,15 +257,38 @@ class BandedEngine:
             out.append(torch.as_tensor(_CudaPlane(ptr, self.local_rows, pitch), device="cuda"))
         return out
 
-    def step(self):
-        self.engine.step()
-        exchange_halos(self.planes(), self.plan, self.group)
+    def step(self, frames=1):
+        if self.exchange == "p2p":
+            if not self.linked:
+                raise RuntimeError("p2p bands must be linked (link / link_ipc) before stepping")
+            self.engine.step_frames(frames)  # halos travel inside the step kernels
+            return
+        for _ in range(frames):
+            self.engine.step()
+            exchange_halos(self.planes(), self.plan, self.group)
 
-    def owned_positions(self):
-        p = self.engine.read_positions()
+    def _owned(self, arr):
         a = (self.plan.j0 - self.plan.l0) * self.nx
         b = (self.plan.j1 - self.plan.l0) * self.nx
-        return p[a:b]
+        return arr[a:b]
+
+    def owned_positions(self):
+        return self._owned(self.engine.read_positions())
+
+    def owned_velocities(self):
+        return self._owned(self.engine.read_velocities())
+
+    def owned_normals(self):
+        return self._owned(self.engine.read_normals())
+
+
+def link_local(bands):
+    """Link the bands of one process (one device) for p2p stepping."""
+    info = [b.buffers() for b in bands]
+    for r, b in enumerate(bands):
+        up = (info[r - 1], bands[r - 1].plan) if r > 0 else None
+        down = (info[r + 1], bands[r + 1].plan) if r + 1 < len(bands) else None
+        b.link(up, down)
 
 
 def run_banded_bench(args, metric):
@@ -168,19 +310,21 @@ def run_banded_bench(args, metric):
     params = SimParams(dt=CONTACT_DT, stiffness=k, damping=c)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    band = BandedEngine(n, n, params, rank, world, stream=stream.cuda_stream)
-    for _ in range(args.warmup):
-        band.step()
+    exchange = os.environ.get("CLOTHSIM_BAND_EXCHANGE", "p2p")
+    band = BandedEngine(n, n, params, rank, world, stream=stream.cuda_stream, exchange=exchange)
+    if exchange == "p2p":
+        band.link_ipc()
+    band.step(args.warmup)
     torch.cuda.synchronize()
     dist.barrier()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
     a.record(stream)
-    for _ in range(args.steps):
-        band.step()
+    band.step(args.steps)
     b.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
+    finite = bool(np.isfinite(band.owned_positions()).all())
     ms = torch.tensor([a.elapsed_time(b) / args.steps], device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
@@ -190,11 +334,18 @@ def run_banded_bench(args, metric):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (hanging 4096^2, dt 0.004)",
-            "config": {"workload": "C5: 4096x4096 hanging cloth, row bands + 2-row NCCL halos",
+            "config": {"workload": "C5: 4096x4096 hanging cloth, row bands with 2-row halos",
                        "nodes": n * n, "parallelism": f"rowband{world}",
+                       "halo_exchange": ("peer stores inside the step kernel + stream-ordered "
+                                         "flag handshake (CUDA IPC over NVLink)"
+                                         if exchange == "p2p" else
+                                         "torch.distributed NCCL send/recv after each step"),
                        "l2": "inputs (16.8M nodes, 805 MB/step) larger than L2"},
             "node_updates_per_s": 1000.0 / ms * n * n,
             "gpu_launches": args.steps * band.engine.kernels_per_frame,
+            "finite": finite,
         }
         print(json.dumps(line))
+    if exchange == "p2p":
+        band.close()
     dist.destroy_process_group()

@@ -6,7 +6,9 @@
 //   [spring_force+integrate] x substeps -> detect A -> detect B -> respond
 //   -> normals                                           (engine.py:304-344)
 // and readbacks return copies in the reference's (N,3) layouts.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <climits>
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
@@ -115,6 +117,17 @@ struct cs_engine {
     cudaEvent_t ev_frame[2] = {nullptr, nullptr}, ev_moved[2] = {nullptr, nullptr};
     float *rec_stage[2] = {nullptr, nullptr};
     int64_t frames = 0;
+    // row band (cs_set_halo_peers): neighbours' buffers + per-pass handshake
+    struct Link {
+        bool on = false;
+        void *state[2] = {nullptr, nullptr};
+        int64_t plane = 0, src_row0 = 0, dst_row0 = 0, rows = 0;
+        uint32_t *remote_flag = nullptr;
+    };
+    bool banded = false;
+    Link up, dn;
+    uint32_t *hflags = nullptr;  // [from up, from down] = force passes that neighbour finished
+    uint32_t passes = 0;         // force passes this engine issued
     StepParams sp{};
     CsrParams cp{};
 
@@ -298,8 +311,110 @@ static void launch_frame(cs_engine *h) {
     h->normals_stale = fuse;
 }
 
+// ---------------------------------------------------------------------------
+// row bands (BASELINE config 5): one engine per GPU holds its owned rows plus
+// a 2-row halo on each side.  The step kernel itself stores each boundary row
+// into the neighbour's halo (peer memory over NVLink: cudaIpc handles across
+// processes, plain pointers within one); a stream-ordered handshake replaces
+// the exchange step -- before force pass t an engine's stream waits until
+// each neighbour has finished pass t-1 (so the halo it reads is complete and
+// the buffer the neighbour writes is no longer being read), and after the
+// pass it bumps its pass count in each neighbour's flag word.  No host
+// synchronisation, no NCCL call and no packing kernel on the data path.
+// ---------------------------------------------------------------------------
+typedef CUresult (*PfnValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static PfnValue32 g_wait32 = nullptr, g_write32 = nullptr;
+
+static int load_memops() {
+    if (g_wait32 && g_write32) return 0;
+    cudaDriverEntryPointQueryResult q1 = cudaDriverEntryPointSymbolNotFound, q2 = q1;
+    CK(cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", (void **)&g_wait32, 12000,
+                                        cudaEnableDefault, &q1));
+    CK(cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", (void **)&g_write32, 12000,
+                                        cudaEnableDefault, &q2));
+    if (q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess || !g_wait32 ||
+        !g_write32) {
+        g_wait32 = g_write32 = nullptr;
+        return fail(CS_E_CUDA, "the driver does not provide cuStreamWaitValue32/cuStreamWriteValue32");
+    }
+    return 0;
+}
+
+#define CU(call)                                                                         \
+    do {                                                                                 \
+        CUresult r_ = (call);                                                            \
+        if (r_ != CUDA_SUCCESS)                                                          \
+            return fail(CS_E_CUDA, std::string(#call) + ": CUresult " + std::to_string((int)r_)); \
+    } while (0)
+
+static int halo_wait(cs_engine *h) {
+    if (h->up.on)
+        CU(g_wait32((CUstream)h->st, (CUdeviceptr)(h->hflags + 0), h->passes, CU_STREAM_WAIT_VALUE_GEQ));
+    if (h->dn.on)
+        CU(g_wait32((CUstream)h->st, (CUdeviceptr)(h->hflags + 1), h->passes, CU_STREAM_WAIT_VALUE_GEQ));
+    return 0;
+}
+
+static int halo_signal(cs_engine *h) {
+    ++h->passes;  // the default write orders the pass's (peer) stores before the flag
+    if (h->up.on)
+        CU(g_write32((CUstream)h->st, (CUdeviceptr)h->up.remote_flag, h->passes, CU_STREAM_WRITE_VALUE_DEFAULT));
+    if (h->dn.on)
+        CU(g_write32((CUstream)h->st, (CUdeviceptr)h->dn.remote_flag, h->passes, CU_STREAM_WRITE_VALUE_DEFAULT));
+    return 0;
+}
+
+// neighbour planes of buffer `dst`, shifted so that local offsets address them
+static HaloDst halo_dst(const cs_engine *h, int dst) {
+    HaloDst d{};
+    auto fill = [&](const cs_engine::Link &L, float **out) {
+        for (int q = 0; q < 6; ++q) {
+            if (!L.on) {
+                out[q] = nullptr;
+                continue;
+            }
+            const int64_t elems = q * L.plane + (L.dst_row0 - L.src_row0) * h->pitch;
+            out[q] = (float *)((intptr_t)L.state[dst] + (intptr_t)(elems * 4));
+        }
+    };
+    fill(h->up, d.up);
+    fill(h->dn, d.dn);
+    return d;
+}
+
+static int banded_frame(cs_engine *h) {
+    const bool fuse = h->fuse_normals();
+    const bool packed = (h->flags & CS_FLAG_PAIRED) != 0;
+    const bool fused_push = !h->fixed && packed;  // k_pair3 stores into the peers itself
+    for (int s = 0; s < h->substeps; ++s) {
+        if (int r = halo_wait(h)) return r;
+        if (s == 0 && !fuse) pass_normals(h);  // the frame's starting state, halo complete
+        const int src = h->cur, dst = 1 - h->cur;
+        const HaloDst hd = halo_dst(h, dst);
+        launch_strip_step(h->sp, h->fixed, fuse && s == 0, (const float *)h->state[src],
+                          (float *)h->state[dst], h->pinbits,
+                          h->has_ext ? (const float *)h->ext : nullptr, (float *)h->normals, h->st,
+                          packed, fused_push ? &hd : nullptr);
+        if (!fused_push) {
+            if (h->up.on)
+                launch_push_rows((const float *)h->state[dst], h->plane, (int)h->pitch,
+                                 (int)h->up.src_row0, (int)(h->up.src_row0 + h->up.rows), hd.up, h->st);
+            if (h->dn.on)
+                launch_push_rows((const float *)h->state[dst], h->plane, (int)h->pitch,
+                                 (int)h->dn.src_row0, (int)(h->dn.src_row0 + h->dn.rows), hd.dn, h->st);
+        }
+        CK(cudaGetLastError());
+        h->cur = dst;
+        if (int r = halo_signal(h)) return r;
+    }
+    h->forces_valid = true;
+    h->normals_stale = true;  // normals trail by one frame; refreshed when read
+    return 0;
+}
+
 static void flush_normals(cs_engine *h) {
     if (h->normals_stale) {
+        if (h->banded) halo_wait(h);  // the neighbours' last pass completes our halo
         pass_normals(h);
         h->normals_stale = false;
     }
@@ -382,6 +497,10 @@ static int build(cs_engine *h, const cs_desc *d) {
     sp.scale_f = (float)d->fixed_point_scale;
     sp.scale_d = (double)d->fixed_point_scale;
     sp.explicit_euler = (d->flags & CS_FLAG_EXPLICIT_EULER) ? 1 : 0;
+    sp.row_lo = 0;
+    sp.row_hi = sp.ny;
+    sp.halo_up_hi = INT_MIN;
+    sp.halo_dn_lo = INT_MAX;
     CsrParams &cp = h->cp;
     cp.n = N;
     cp.plane = P;
@@ -567,7 +686,7 @@ extern "C" int cs_destroy(cs_engine *h) {
                     h->pinned8, h->ext, h->forces_raw, h->csr_off, h->csr_nbr, h->csr_kind,
                     h->csr_rest, h->csr_rest64, h->inc_off, h->inc_tri, h->face, h->tris_g,
                     h->edges_g, h->corners, h->onormals, h->acc, h->count, h->touched,
-                    h->touched_n, h->stats, h->stage};
+                    h->touched_n, h->stats, h->stage, h->hflags};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (h->has_obstacle) free_broadphase(h->bp);
@@ -619,6 +738,13 @@ extern "C" int cs_create(const cs_desc *d, cs_engine **out) {
 // ---------------------------------------------------------------------------
 extern "C" int cs_step(cs_engine *h, int32_t frames) {
     if (!h) return fail(CS_E_INVALID, "null engine");
+    if (h->banded) {  // per-pass handshake values change every frame: no graph
+        for (int32_t f = 0; f < frames; ++f) {
+            if (int r = banded_frame(h)) return r;
+            h->frames++;
+        }
+        return 0;
+    }
     for (int32_t f = 0; f < frames; ++f) {
         if (h->use_graph) {
             const int start = h->cur;
@@ -803,6 +929,9 @@ extern "C" int cs_read(cs_engine *h, int32_t id, void *dst) {
         case CS_BUF_PREV_POSITIONS:
         case CS_BUF_NORMALS: {
             if (id == CS_BUF_NORMALS) flush_normals(h);
+            if (h->banded) {
+                if (int r = halo_wait(h)) return r;  // halo rows of the current state landed
+            }
             const void *base = id == CS_BUF_NORMALS ? h->normals
                                : id == CS_BUF_PREV_POSITIONS ? h->state[1 - h->cur]
                                                              : h->state[h->cur];
@@ -941,6 +1070,91 @@ extern "C" int cs_state_plane(cs_engine *h, int32_t which, void **ptr, int64_t *
     if (!h || !ptr || which < 0 || which > 5) return fail(CS_E_INVALID, "bad argument");
     *ptr = (char *)h->state[h->cur] + (size_t)which * h->plane * h->esz;
     if (pitch) *pitch = h->pitch;
+    return 0;
+}
+
+// ---- row bands -------------------------------------------------------------
+extern "C" int cs_state_buffers(cs_engine *h, void **state0, void **state1, uint32_t **flags,
+                                int64_t *plane, int64_t *pitch) {
+    if (!h) return fail(CS_E_INVALID, "null engine");
+    if (!h->hflags) {
+        CK(dalloc(&h->hflags, 2));
+        CK(cudaMemset(h->hflags, 0, 2 * sizeof(uint32_t)));
+    }
+    if (state0) *state0 = h->state[0];
+    if (state1) *state1 = h->state[1];
+    if (flags) *flags = h->hflags;
+    if (plane) *plane = h->plane;
+    if (pitch) *pitch = h->pitch;
+    return 0;
+}
+
+extern "C" int cs_set_halo_peers(cs_engine *h, int64_t row_lo, int64_t row_hi,
+                                 const cs_halo_peer *up, const cs_halo_peer *down) {
+    if (!h) return fail(CS_E_INVALID, "null engine");
+    if (!h->grid || !h->strip || h->fp64)
+        return fail(CS_E_INVALID, "row bands need the float32 grid strip path");
+    if (h->has_obstacle) return fail(CS_E_INVALID, "collision across row bands is not supported");
+    if (h->frames != 0 || h->cur != 0)
+        return fail(CS_E_INVALID, "link row bands before the first frame (lockstep parity)");
+    if (row_lo < 0 || row_hi > h->rows || row_lo >= row_hi)
+        return fail(CS_E_INVALID, "owned rows out of range");
+    if (int r = load_memops()) return r;
+    if (int r = cs_state_buffers(h, nullptr, nullptr, nullptr, nullptr, nullptr)) return r;
+    auto set = [&](cs_engine::Link &L, const cs_halo_peer *p) -> int {
+        L = cs_engine::Link{};
+        if (!p) return 0;
+        if (!p->state[0] || !p->state[1] || !p->remote_flag || p->rows < 1 || p->plane < 1)
+            return fail(CS_E_INVALID, "incomplete halo peer");
+        if (p->src_row0 < row_lo || p->src_row0 + p->rows > row_hi)
+            return fail(CS_E_INVALID, "halo rows sent must be owned rows");
+        L.on = true;
+        L.state[0] = p->state[0];
+        L.state[1] = p->state[1];
+        L.plane = p->plane;
+        L.src_row0 = p->src_row0;
+        L.dst_row0 = p->dst_row0;
+        L.rows = p->rows;
+        L.remote_flag = p->remote_flag;
+        return 0;
+    };
+    if (int r = set(h->up, up)) return r;
+    if (int r = set(h->dn, down)) return r;
+    if (h->up.on && h->up.src_row0 != row_lo)
+        return fail(CS_E_INVALID, "rows sent up must start at the first owned row");
+    if (h->dn.on && h->dn.src_row0 + h->dn.rows != row_hi)
+        return fail(CS_E_INVALID, "rows sent down must end at the last owned row");
+    CK(cudaStreamSynchronize(h->st));
+    h->sp.row_lo = (int)row_lo;
+    h->sp.row_hi = (int)row_hi;
+    h->sp.halo_up_hi = h->up.on ? (int)(h->up.src_row0 + h->up.rows) : INT_MIN;
+    h->sp.halo_dn_lo = h->dn.on ? (int)h->dn.src_row0 : INT_MAX;
+    h->banded = true;
+    h->passes = 0;
+    drop_graphs(h);
+    return 0;
+}
+
+extern "C" int cs_ipc_export(void *dev_ptr, uint8_t handle[64]) {
+    if (!dev_ptr || !handle) return fail(CS_E_INVALID, "null argument");
+    cudaIpcMemHandle_t hd;
+    CK(cudaIpcGetMemHandle(&hd, dev_ptr));
+    static_assert(sizeof(hd) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    memcpy(handle, &hd, 64);
+    return 0;
+}
+
+extern "C" int cs_ipc_open(const uint8_t handle[64], void **dev_ptr) {
+    if (!handle || !dev_ptr) return fail(CS_E_INVALID, "null argument");
+    cudaIpcMemHandle_t hd;
+    memcpy(&hd, handle, 64);
+    CK(cudaIpcOpenMemHandle(dev_ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+    return 0;
+}
+
+extern "C" int cs_ipc_close(void *dev_ptr) {
+    if (!dev_ptr) return fail(CS_E_INVALID, "null argument");
+    CK(cudaIpcCloseMemHandle(dev_ptr));
     return 0;
 }
 

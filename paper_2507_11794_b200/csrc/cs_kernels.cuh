@@ -168,11 +168,23 @@ void launch_csr_normals_f64(int64_t n, int64_t P, int64_t nc, const double *pos,
 // ---- launchers (defined in the .cu files) -------------------------------------
 void launch_grid_step(const StepParams &p, bool fixed, const float *src, float *dst,
                       const uint32_t *pinbits, const float *ext, cudaStream_t st);
+// A row band's neighbour planes (x y z vx vy vz of the neighbour's
+// destination state buffer), each pre-shifted by (dst_row0 - src_row0) rows
+// so that the LOCAL element offset of a boundary node addresses its halo
+// copy on the neighbour (NVLink peer memory, or the same device in tests).
+struct HaloDst {
+    float *up[6];
+    float *dn[6];
+};
 void launch_strip_step(const StepParams &p, bool fixed, bool normals, const float *src,
                        float *dst, const uint32_t *pinbits, const float *ext, float *nrm,
-                       cudaStream_t st, bool packed = false);
+                       cudaStream_t st, bool packed = false, const HaloDst *halo = nullptr);
 void launch_pair3_step(const StepParams &p, bool normals, const float *src, float *dst,
-                       const uint32_t *pinbits, const float *ext, float *nrm, cudaStream_t st);
+                       const uint32_t *pinbits, const float *ext, float *nrm, cudaStream_t st,
+                       const HaloDst *halo = nullptr);
+// copy rows [r0, r1) of the six planes of `src` to the (pre-shifted) planes `to`
+void launch_push_rows(const float *src, int64_t plane, int pitch, int r0, int r1,
+                      float *const to[6], cudaStream_t st);
 void launch_pair_normals(const StepParams &p, const float *state, float *nrm, cudaStream_t st);
 int pair3_rows(const StepParams &p);
 void launch_grid_forces(const StepParams &p, const float *src, int32_t *forces, cudaStream_t st);

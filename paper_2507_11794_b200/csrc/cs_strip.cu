@@ -163,9 +163,9 @@ k_strip_step(const StepParams p, const float *__restrict__ src, float *__restric
     const int warp = blockIdx.x * SWPB + (threadIdx.x >> 5);
     const int strips_x = (p.nx + SO - 1) / SO;
     const int sx = warp % strips_x, sy = warp / strips_x;
-    const int y0 = sy * p.strip_h;
-    if (y0 >= p.ny) return;  // whole warp exits together
-    const int y1 = min(y0 + p.strip_h, p.ny);
+    const int y0 = p.row_lo + sy * p.strip_h;
+    if (y0 >= p.row_hi) return;  // whole warp exits together
+    const int y1 = min(y0 + p.strip_h, p.row_hi);
     const int i = sx * SO - 2 + lane;
     const bool col_ok = (i >= 0) & (i < p.nx);
     const bool out_lane = (lane >= 2) & (lane < 30) & col_ok;
@@ -282,9 +282,9 @@ k_strip_step(const StepParams p, const float *__restrict__ src, float *__restric
 
 void launch_strip_step(const StepParams &p, bool fixed, bool normals, const float *src,
                        float *dst, const uint32_t *pinbits, const float *ext, float *nrm,
-                       cudaStream_t st, bool packed) {
+                       cudaStream_t st, bool packed, const HaloDst *halo) {
     if (!fixed && packed) {  // paired-column f32x2 kernel: cs_pair3.cu
-        launch_pair3_step(p, normals, src, dst, pinbits, ext, nrm, st);
+        launch_pair3_step(p, normals, src, dst, pinbits, ext, nrm, st, halo);
         return;
     }
     // Tall strips amortise the 2-row vertical halo; small grids get shorter
@@ -292,10 +292,12 @@ void launch_strip_step(const StepParams &p, bool fixed, bool normals, const floa
     const int sxn = (p.nx + SO - 1) / SO;
     const dim3 block(SW * SWPB);
     int sh = SH_MAX;
-    while (sh > 8 && (int64_t)sxn * ((p.ny + sh - 1) / sh) < 148 * 16) sh /= 2;
+    const int rows = p.row_hi - p.row_lo;
+    while (sh > 8 && (int64_t)sxn * ((rows + sh - 1) / sh) < 148 * 16) sh /= 2;
     StepParams q = p;
     q.strip_h = sh;
-    const int64_t strips = (int64_t)sxn * ((p.ny + sh - 1) / sh);
+    const int64_t strips = (int64_t)sxn * ((rows + sh - 1) / sh);
+    if (strips <= 0) return;
     const unsigned blocks = (unsigned)((strips + SWPB - 1) / SWPB);
     if (fixed) {
         if (normals) k_strip_step<true, true><<<blocks, block, 0, st>>>(q, src, dst, pinbits, ext, nrm);

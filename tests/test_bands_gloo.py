@@ -98,3 +98,23 @@ def test_grid_band_matches_global_grid_rows():
     np.testing.assert_array_equal(b.masses, g.masses[3 * 7:9 * 7])
     assert set(np.unique(b.spring_rest_lengths.astype(np.float32))) <= \
         set(np.unique(g.spring_rest_lengths.astype(np.float32)))
+
+
+@pytest.mark.parametrize("ny,world", [(64, 2), (97, 3), (4096, 8), (10, 4)])
+def test_peer_rows_land_on_the_neighbours_halo(ny, world):
+    """The p2p link (bands.peer_rows): the local rows a band stores into each
+    neighbour are exactly the global rows that neighbour's halo holds."""
+    from paper_2507_11794_b200.bands import peer_rows
+
+    plans = [HaloPlan(ny, world, r) for r in range(world)]
+    for r, me in enumerate(plans):
+        for direction, q in (("up", r - 1), ("down", r + 1)):
+            if not 0 <= q < world:
+                continue
+            nb = plans[q]
+            src, dst, rows = peer_rows(me, nb, direction)
+            assert rows == 2
+            assert me.j0 <= me.l0 + src and me.l0 + src + rows <= me.j1  # owned rows
+            assert me.l0 + src == nb.l0 + dst  # same global rows
+            halo = nb.recv_down if direction == "up" else nb.recv_up
+            assert (dst, dst + rows) == halo

@@ -106,3 +106,46 @@ def test_c3_drapes_finite_with_contacts_in_both_modes():
         r = np.linalg.norm(pos.astype(np.float64), axis=1)
         assert (r > 0.27).mean() > 0.999
     assert abs(hits["fast"] - hits["fixed"]) / hits["fixed"] < 0.05
+
+
+@pytest.mark.parametrize("world,precision,n,normals", [
+    (2, "fast", 160, "auto"), (3, "fast", 161, "auto"), (3, "fast", 130, "split"),
+    (4, "fixed", 96, "auto"), (2, "fast", 64, "fused"),
+])
+def test_p2p_bands_bit_identical_to_one_engine(world, precision, n, normals):
+    """Row bands linked by peer stores inside the step kernel (the NVLink
+    path of bench.py --gpus N), several bands on one device, each on its own
+    stream, ordered only by the stream flag handshake: owned rows equal the
+    single-engine run bit for bit (positions, velocities, normals)."""
+    from paper_2507_11794_b200.bands import link_local
+
+    k, c = stable_coefficients(NODE_MASS, CONTACT_DT)
+    params = P.SimParams(dt=CONTACT_DT, stiffness=k, damping=c)
+    whole = P.Engine(P.build_scene(P.ScenarioConfig("hanging", (n, n), dt=CONTACT_DT)).mesh,
+                     params=params, precision=precision, normals=normals)
+    bands = [BandedEngine(n, n, params, r, world, exchange="p2p", precision=precision,
+                          normals=normals) for r in range(world)]
+    link_local(bands)
+    for chunk in (1, 7, 22):  # 30 frames, enqueued band after band
+        whole.step_frames(chunk)
+        for b in bands:
+            b.step(chunk)
+    for what in ("positions", "velocities", "normals"):
+        got = np.concatenate([getattr(b, f"owned_{what}")() for b in bands])
+        np.testing.assert_array_equal(got, getattr(whole, f"read_{what}")(), err_msg=what)
+    for b in bands:
+        b.close()
+
+
+def test_p2p_link_validation():
+    from paper_2507_11794_b200 import _native as N  # noqa: F401
+    from paper_2507_11794_b200.bands import link_local
+
+    k, c = stable_coefficients(NODE_MASS, CONTACT_DT)
+    params = P.SimParams(dt=CONTACT_DT, stiffness=k, damping=c)
+    bands = [BandedEngine(64, 64, params, r, 2, exchange="p2p") for r in range(2)]
+    with pytest.raises(RuntimeError):
+        bands[0].step()  # not linked
+    bands[0].engine.step()  # a frame before linking breaks lockstep parity
+    with pytest.raises(ValueError):
+        link_local(bands)

@@ -42,7 +42,9 @@ def test_descriptor_layout_matches_c(tmp_path):
     src.write_text(
         "#include <stdio.h>\n#include <stddef.h>\n#include \"clothsim_b200.h\"\n"
         "int main(void){\n" + body + '\nprintf("sizeof %zu\\n", sizeof(cs_desc));'
-        '\nprintf("stats %zu\\n", sizeof(cs_stats));\nreturn 0;}\n')
+        '\nprintf("stats %zu\\n", sizeof(cs_stats));'
+        '\nprintf("peer %zu\\n", sizeof(cs_halo_peer));'
+        '\nprintf("peer_flag %zu\\n", offsetof(cs_halo_peer, remote_flag));\nreturn 0;}\n')
     exe = tmp_path / "layout"
     cc = "/usr/bin/gcc" if os.path.exists("/usr/bin/gcc") else "gcc"
     subprocess.run([cc, "-I", os.path.dirname(HEADER), str(src), "-o", str(exe)], check=True)
@@ -52,6 +54,8 @@ def test_descriptor_layout_matches_c(tmp_path):
         assert int(out[f]) == getattr(N.CsDesc, f).offset, f
     assert int(out["sizeof"]) == ctypes.sizeof(N.CsDesc)
     assert int(out["stats"]) == ctypes.sizeof(N.CsStats)
+    assert int(out["peer"]) == ctypes.sizeof(N.CsHaloPeer)
+    assert int(out["peer_flag"]) == N.CsHaloPeer.remote_flag.offset
 
 
 def test_adapter_none_is_refused(monkeypatch):
