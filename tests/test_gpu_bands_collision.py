@@ -149,3 +149,15 @@ def test_p2p_link_validation():
     bands[0].engine.step()  # a frame before linking breaks lockstep parity
     with pytest.raises(ValueError):
         link_local(bands)
+
+
+def test_ipc_linked_bands_across_processes():
+    """The multi-process link (CUDA IPC handles swapped over torch.distributed,
+    as bench.py --gpus N does across GPUs), two processes on one device."""
+    import subprocess
+    import sys
+
+    root = __import__("os").path.dirname(__import__("os").path.dirname(__file__))
+    res = subprocess.run([sys.executable, "tools/ipc_bands_smoke.py", "192", "2"], cwd=root,
+                         capture_output=True, text=True, timeout=280)
+    assert res.returncode == 0 and "'ok'" in res.stdout, res.stdout + res.stderr[-2000:]
