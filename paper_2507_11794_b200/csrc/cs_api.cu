@@ -85,16 +85,14 @@ struct cs_engine {
     bool strip = true;          // grid path uses the warp-strip kernel (cs_strip.cu)
     // The strip kernel can compute the previous frame's normals in the same
     // pass (fused: one launch per frame, 60 B/node) or a stand-alone normals
-    // kernel can follow it (split: 72 B/node).  Measured on B200: fused wins
-    // while a frame is latency-bound (C2, 640K nodes: 24.6 vs 28.7 us), split
-    // wins once it is throughput-bound (C5, 16.8M: 330 vs 343 us) -- the fused
-    // kernel needs 168 registers, the pair 128 + 88.  Default: fused up to
-    // 2M nodes; CS_FLAG_FUSE_NORMALS / CS_FLAG_SPLIT_NORMALS force a choice.
+    // kernel can follow it (split: 72 B/node).  Measured on B200 with
+    // k_pair3: fused 24.6 vs split 26.6 us at C2 (640K nodes) and 297.5 vs
+    // 315.5 us at C5 (16.8M) -- fused is the default at every size;
+    // CS_FLAG_SPLIT_NORMALS forces the split pair (k_pair3 + k_pair_normals).
     bool fuse_normals() const {
         if (!(grid && strip)) return false;
         if (flags & CS_FLAG_SPLIT_NORMALS) return false;
-        if (flags & CS_FLAG_FUSE_NORMALS) return true;
-        return fixed || !(flags & CS_FLAG_PAIRED) || N <= (int64_t)1 << 21;
+        return true;
     }
     bool normals_stale = false; // normals buffer holds the previous frame's (fused)
     float *corners = nullptr, *onormals = nullptr;
