@@ -33,7 +33,8 @@ import numpy as np
 from . import _native as N
 from .errors import AdapterUnavailable, CapacityError, CollisionBudgetError
 from .fixedpoint import encode_values
-from .mesh import SimParams, grid_springs, grid_triangles, grid_unique_edges, unique_edges
+from .mesh import (SimParams, grid_families, grid_springs, grid_triangles, grid_unique_edges,
+                   unique_edges)
 
 __all__ = [
     "ADAPTER_ENV", "CudaDevice", "get_adapter", "Engine", "StepResult", "Layout",
@@ -192,13 +193,16 @@ def _grid_stencil_rest(mesh):
     if not np.array_equal(np.asarray(mesh.triangles), grid_triangles(nx, ny)):
         return None
     rest32 = np.asarray(mesh.spring_rest_lengths).astype(_F32)
-    off = springs[:, 1].astype(np.int64) - springs[:, 0]
     rest6 = []
-    for kind, delta in ((0, 1), (0, nx), (1, nx + 1), (1, nx - 1), (2, 2), (2, 2 * nx)):
-        vals = np.unique(rest32[(kinds == kind) & (off == delta)])
-        if len(vals) > 1:
+    for views in grid_families(rest32, nx, ny):  # +i, +j, shear +nx+1, +nx-1, bend +2, +2nx
+        vals = [v for v in views if v.size]
+        if not vals:
+            rest6.append(0.0)
+            continue
+        lo, hi = min(float(v.min()) for v in vals), max(float(v.max()) for v in vals)
+        if lo != hi:  # one f32 rest length per family, else no stencil
             return None
-        rest6.append(float(vals[0]) if len(vals) else 0.0)
+        rest6.append(lo)
     return nx, ny, rest6
 
 
@@ -242,12 +246,18 @@ class Engine:
         n = int(len(np.asarray(mesh.positions)))
         tris = np.ascontiguousarray(mesh.triangles, dtype=np.int32)
         stencil = _grid_stencil_rest(mesh)
-        if stencil is not None:
-            edges = grid_unique_edges(stencil[0], stencil[1])
-        else:
-            edges = unique_edges(tris) if len(tris) else np.zeros((0, 2), np.int32)
         has_obs = obstacle is not None and len(obstacle.triangles) > 0
         n_obs = len(obstacle.triangles) if obstacle is not None else 0
+        # the unique cloth edges feed only the collision passes
+        if stencil is not None:
+            gx, gy = stencil[0], stencil[1]
+            n_edges = (gx - 1) * gy + gx * (gy - 1) + (gx - 1) * (gy - 1)
+            edges = grid_unique_edges(gx, gy) if has_obs else np.zeros((0, 2), np.int32)
+        else:
+            edges = unique_edges(tris) if len(tris) else np.zeros((0, 2), np.int32)
+            n_edges = len(edges)
+            if not has_obs:
+                edges = np.zeros((0, 2), np.int32)
         springs = np.ascontiguousarray(mesh.spring_indices, dtype=np.int32).reshape(-1, 2)
         esz = 8 if precision == "fp64" else 4
         pitch_nodes = ((stencil[0] + 31) // 32 * 32) * stencil[1] if stencil else n
@@ -256,12 +266,12 @@ class Engine:
             + 8 * len(edges) + 48 * n_obs
         if stencil is None:
             total += 16 * len(springs) * 2 + 8 * n + 12 * len(tris) + 12 * len(tris) * esz
-        self.layout = Layout(n, len(springs), len(tris), len(edges), n_obs, state_bytes, total)
+        self.layout = Layout(n, len(springs), len(tris), n_edges, n_obs, state_bytes, total)
         free, _ = self.device.mem_info()
         self.layout.validate(free)
 
         # collision.py:258-266 / engine.py:137-142: same census, same refusal
-        self.pairs_per_frame = len(edges) * n_obs + 3 * n_obs * len(tris)
+        self.pairs_per_frame = n_edges * n_obs + 3 * n_obs * len(tris)
         if self.pairs_per_frame > pair_budget:
             raise CollisionBudgetError(
                 f"frame needs {self.pairs_per_frame} edge-triangle tests, "

@@ -167,39 +167,166 @@ def _interleave(cands):
 
 
 def grid_springs(nx: int, ny: int):
-    """(S,2) int32 endpoints and (S,) int32 kinds in the reference order."""
-    j, i = np.divmod(np.arange(nx * ny, dtype=np.int64), nx)
-    n = j * nx + i
-    sa, sb = _interleave([(n, n + 1, i + 1 < nx), (n, n + nx, j + 1 < ny)])
-    cj, ci = np.divmod(np.arange((nx - 1) * (ny - 1), dtype=np.int64), nx - 1)
-    c = cj * nx + ci
-    ones = np.ones_like(c, dtype=bool)
-    ha, hb = _interleave([(c, c + nx + 1, ones), (c + 1, c + nx, ones)])
-    ba, bb = _interleave([(n, n + 2, i + 2 < nx), (n, n + 2 * nx, j + 2 < ny)])
-    pairs = np.stack([np.concatenate([sa, ha, ba]), np.concatenate([sb, hb, bb])], axis=1)
-    kinds = np.concatenate([np.zeros(len(sa), np.int32), np.ones(len(ha), np.int32),
-                            np.full(len(ba), 2, np.int32)])
-    return pairs.astype(np.int32), kinds
+    """(S,2) int32 endpoints and (S,) int32 kinds in the reference order
+    (mesh.py:274-289): per node (row-major) structural +i then +j; per cell
+    the two shears; per node bend +2i then +2j -- built row block by row
+    block straight into int32 (no per-spring Python, no int64 temporaries)."""
+    i32 = np.int32
+    cols = np.arange(nx, dtype=i32)
+    base = (np.arange(ny, dtype=i32) * i32(nx))[:, None]
+    # structural: rows j < ny-1 hold 2(nx-1)+1 springs, the last row nx-1
+    st = np.empty((ny - 1, 2 * nx - 1, 2), i32)
+    st[:, 0:2 * nx - 2:2, 0] = base[:-1] + cols[:-1]
+    st[:, 0:2 * nx - 2:2, 1] = base[:-1] + cols[:-1] + 1
+    st[:, 1:2 * nx - 2:2, 0] = base[:-1] + cols[:-1]
+    st[:, 1:2 * nx - 2:2, 1] = base[:-1] + cols[:-1] + nx
+    st[:, 2 * nx - 2, 0] = base[:-1, 0] + nx - 1
+    st[:, 2 * nx - 2, 1] = base[:-1, 0] + 2 * nx - 1
+    last = np.stack([base[-1, 0] + cols[:-1], base[-1, 0] + cols[:-1] + 1], axis=1)
+    # shear: per cell (c, c+nx+1), (c+1, c+nx)
+    c = base[:-1] + cols[:-1]
+    sh = np.empty((ny - 1, nx - 1, 2, 2), i32)
+    sh[:, :, 0, 0] = c
+    sh[:, :, 0, 1] = c + nx + 1
+    sh[:, :, 1, 0] = c + 1
+    sh[:, :, 1, 1] = c + nx
+    # bend: rows j < ny-2 hold 2(nx-2)+2 springs, the last two rows nx-2 each
+    m = max(nx - 2, 0)
+    bd = np.empty((max(ny - 2, 0), 2 * m + min(nx, 2), 2), i32)
+    if ny > 2:
+        b0 = base[:-2]
+        bd[:, 0:2 * m:2, 0] = b0 + cols[:m]
+        bd[:, 0:2 * m:2, 1] = b0 + cols[:m] + 2
+        bd[:, 1:2 * m:2, 0] = b0 + cols[:m]
+        bd[:, 1:2 * m:2, 1] = b0 + cols[:m] + 2 * nx
+        tail = cols[m:]
+        bd[:, 2 * m:, 0] = b0 + tail
+        bd[:, 2 * m:, 1] = b0 + tail + 2 * nx
+    tail_rows = base[max(ny - 2, 0):]
+    bl = np.stack([(tail_rows + cols[:m]).ravel(), (tail_rows + cols[:m] + 2).ravel()], axis=1)
+    pairs = np.concatenate([st.reshape(-1, 2), last, sh.reshape(-1, 2), bd.reshape(-1, 2),
+                            bl.astype(i32)])
+    n_st = st.shape[0] * st.shape[1] + len(last)
+    n_sh = sh.shape[0] * sh.shape[1] * 2
+    kinds = np.empty(len(pairs), i32)
+    kinds[:n_st] = 0
+    kinds[n_st:n_st + n_sh] = 1
+    kinds[n_st + n_sh:] = 2
+    return pairs, kinds
+
+
+def grid_families(per_spring, nx: int, ny: int):
+    """Views of a per-spring array laid out in grid_springs order, grouped by
+    stencil family: [+i], [+j], [shear +nx+1], [shear +nx-1], [bend +2],
+    [bend +2nx] -- each a list of strided views (no masks, no copies)."""
+    m = max(nx - 2, 0)
+    n_st = (ny - 1) * (2 * nx - 1)
+    st = per_spring[:n_st].reshape(ny - 1, 2 * nx - 1)
+    o = n_st
+    last = per_spring[o:o + nx - 1]
+    o += nx - 1
+    n_sh = (ny - 1) * (nx - 1) * 2
+    sh = per_spring[o:o + n_sh].reshape(ny - 1, nx - 1, 2)
+    o += n_sh
+    w = 2 * m + min(nx, 2)
+    n_bd = max(ny - 2, 0) * w
+    bd = per_spring[o:o + n_bd].reshape(max(ny - 2, 0), w)
+    o += n_bd
+    bl = per_spring[o:]
+    return ([st[:, 0:2 * nx - 2:2], last], [st[:, 1:2 * nx - 2:2], st[:, 2 * nx - 2]],
+            [sh[:, :, 0]], [sh[:, :, 1]], [bd[:, 0:2 * m:2], bl], [bd[:, 1:2 * m:2], bd[:, 2 * m:]])
 
 
 def grid_triangles(nx: int, ny: int) -> np.ndarray:
     """(C,3) int32: per cell (v00, v01, v10), (v10, v01, v11) (mesh.py:296-305)."""
-    cj, ci = np.divmod(np.arange((nx - 1) * (ny - 1), dtype=np.int64), nx - 1)
-    v00 = cj * nx + ci
-    v10, v01, v11 = v00 + 1, v00 + nx, v00 + nx + 1
-    t = np.stack([np.stack([v00, v01, v10], 1), np.stack([v10, v01, v11], 1)], axis=1)
-    return t.reshape(-1, 3).astype(np.int32)
+    i32 = np.int32
+    v00 = (np.arange(ny - 1, dtype=i32) * i32(nx))[:, None] + np.arange(nx - 1, dtype=i32)
+    t = np.empty((ny - 1, nx - 1, 2, 3), i32)
+    t[..., 0, 0] = v00
+    t[..., 0, 1] = v00 + nx
+    t[..., 0, 2] = v00 + 1
+    t[..., 1, 0] = v00 + 1
+    t[..., 1, 1] = v00 + nx
+    t[..., 1, 2] = v00 + nx + 1
+    return t.reshape(-1, 3)
 
 
 def grid_unique_edges(nx: int, ny: int) -> np.ndarray:
     """unique_edges(grid_triangles(nx, ny)) in closed form: node a's edges to
     larger indices are a+1 (if i < nx-1), a+nx-1 (the cell diagonal v10-v01,
     if i > 0 and j < ny-1) and a+nx (if j < ny-1), already in sorted order."""
-    j, i = np.divmod(np.arange(nx * ny, dtype=np.int64), nx)
-    n = j * nx + i
-    a, b = _interleave([(n, n + 1, i + 1 < nx), (n, n + nx - 1, (i > 0) & (j + 1 < ny)),
-                        (n, n + nx, j + 1 < ny)])
-    return np.stack([a, b], axis=1).astype(np.int32)
+    i32 = np.int32
+    cols = np.arange(nx, dtype=i32)
+    base = (np.arange(ny, dtype=i32) * i32(nx))[:, None]
+    # rows j < ny-1: node 0 has (+1, +nx); nodes 1..nx-2 (+1, +nx-1, +nx);
+    # node nx-1 (+nx-1, +nx) -> 3nx-2 edges per row; the last row nx-1
+    e = np.empty((ny - 1, 3 * nx - 2, 2), i32)
+    b0 = base[:-1, 0][:, None]
+    e[:, 0, 0] = b0[:, 0]
+    e[:, 0, 1] = b0[:, 0] + 1
+    e[:, 1, 0] = b0[:, 0]
+    e[:, 1, 1] = b0[:, 0] + nx
+    mid = cols[1:nx - 1]
+    if len(mid):
+        e[:, 2:3 * nx - 4:3, 0] = b0 + mid
+        e[:, 2:3 * nx - 4:3, 1] = b0 + mid + 1
+        e[:, 3:3 * nx - 4:3, 0] = b0 + mid
+        e[:, 3:3 * nx - 4:3, 1] = b0 + mid + nx - 1
+        e[:, 4:3 * nx - 4:3, 0] = b0 + mid
+        e[:, 4:3 * nx - 4:3, 1] = b0 + mid + nx
+    e[:, 3 * nx - 4, 0] = b0[:, 0] + nx - 1
+    e[:, 3 * nx - 4, 1] = b0[:, 0] + 2 * nx - 2
+    e[:, 3 * nx - 3, 0] = b0[:, 0] + nx - 1
+    e[:, 3 * nx - 3, 1] = b0[:, 0] + 2 * nx - 1
+    last = np.stack([base[-1, 0] + cols[:-1], base[-1, 0] + cols[:-1] + 1], axis=1)
+    return np.concatenate([e.reshape(-1, 2), last.astype(i32)])
+
+
+def _grid_rest(xs, zs):
+    """Rest lengths of grid_springs(len(xs), len(zs)) for the separable grid
+    positions (xs[i], 0, zs[j]) of generate_cloth_grid, in the same block
+    order and with the same float64 arithmetic as |p_b - p_a| =
+    sqrt((dx^2 + dy^2) + dz^2) (mesh.py:293-294), dy = 0 -- from per-column
+    and per-row tables instead of 100M-entry gathers."""
+    nx, ny = len(xs), len(zs)
+    z0 = np.zeros(1)
+
+    def norm(dx, dz):
+        return np.sqrt((dx * dx + z0 * z0) + dz * dz)
+
+    ri = norm(xs[1:] - xs[:-1], z0)                    # struct +i, by i
+    rj = norm(z0, zs[1:] - zs[:-1])                    # struct +j, by j
+    rs = norm((xs[1:] - xs[:-1])[None, :], (zs[1:] - zs[:-1])[:, None])  # shears, by (j, i)
+    m = max(nx - 2, 0)
+    rbi = norm(xs[2:] - xs[:-2], z0) if m else np.zeros(0)   # bend +2i, by i
+    rbj = norm(z0, zs[2:] - zs[:-2]) if ny > 2 else np.zeros(0)  # bend +2j, by j
+    st = np.empty((ny - 1, 2 * nx - 1))
+    st[:, 0:2 * nx - 2:2] = ri[None, :]
+    st[:, 1:2 * nx - 2:2] = rj[:, None]
+    st[:, 2 * nx - 2] = rj
+    sh = np.empty((ny - 1, nx - 1, 2))
+    sh[:, :, 0] = rs
+    sh[:, :, 1] = rs  # (c+1 -> c+nx): dx = -(xs[i+1]-xs[i]), same square
+    bd = np.empty((max(ny - 2, 0), 2 * m + min(nx, 2)))
+    if ny > 2:
+        bd[:, 0:2 * m:2] = rbi[None, :]
+        bd[:, 1:2 * m:2] = rbj[:, None]
+        bd[:, 2 * m:] = rbj[:, None]
+    bl = np.tile(rbi, min(ny, 2))
+    return np.concatenate([st.ravel(), ri, sh.ravel(), bd.ravel(), bl])
+
+
+def _rest_lengths(positions, springs):
+    """|p_b - p_a| in float64 with numpy's norm arithmetic ((dx^2+dy^2)+dz^2,
+    no contraction) -- column by column instead of an (S,3) temporary."""
+    a, b = springs[:, 0], springs[:, 1]
+    acc = None
+    for q in range(3):
+        col = positions[:, q]
+        d = col[b] - col[a]
+        d *= d
+        acc = d if acc is None else np.add(acc, d, out=acc)
+    return np.sqrt(acc, out=acc)
 
 
 def generate_cloth_grid(nx: int, ny: int, width: float = 1.0, height: float = 1.0,
@@ -222,8 +349,7 @@ def generate_cloth_grid(nx: int, ny: int, width: float = 1.0, height: float = 1.
     for j in _resolve_pinned_rows(pinned_rows, ny):
         pinned[j * nx:(j + 1) * nx] = True
     springs, kinds = grid_springs(nx, ny)
-    delta = positions[springs[:, 1]] - positions[springs[:, 0]]
-    rest = np.linalg.norm(delta, axis=1)
+    rest = _grid_rest(np.linspace(0.0, width, nx), np.linspace(0.0, height, ny))
     return ClothMesh(nx=nx, ny=ny, positions=positions, masses=masses, pinned=pinned,
                      spring_indices=springs, spring_rest_lengths=rest, spring_kinds=kinds,
                      triangles=grid_triangles(nx, ny))
@@ -251,7 +377,7 @@ def grid_band(nx: int, ny: int, j0: int, j1: int, width: float = 1.0, height: fl
         if j0 <= j < j1:
             pinned[(j - j0) * nx:(j - j0 + 1) * nx] = True
     springs, kinds = grid_springs(nx, lny)
-    rest = np.linalg.norm(positions[springs[:, 1]] - positions[springs[:, 0]], axis=1)
+    rest = _grid_rest(np.linspace(0.0, width, nx), np.linspace(0.0, height, ny)[j0:j1])
     return ClothMesh(nx=nx, ny=lny, positions=positions, masses=masses, pinned=pinned,
                      spring_indices=springs, spring_rest_lengths=rest, spring_kinds=kinds,
                      triangles=grid_triangles(nx, lny))

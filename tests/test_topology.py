@@ -100,3 +100,33 @@ def test_baseline_scenes_shapes():
     assert c1.mesh.pinned[0] and c1.mesh.pinned[63]
     c4 = baseline_scene("C4")
     assert c4.obstacle.num_triangles == 99904 and c4.params.dt == 0.004
+
+
+@pytest.mark.parametrize("nx,ny", [(2, 2), (2, 7), (7, 2), (3, 3), (31, 17), (64, 64)])
+def test_separable_rest_lengths_equal_per_spring_norm(nx, ny):
+    """mesh._grid_rest (tables per column / row) == |p_b - p_a| per spring."""
+    m = M.generate_cloth_grid(nx, ny, 1.3, 0.7)
+    ref = np.linalg.norm(m.positions[m.spring_indices[:, 1]] - m.positions[m.spring_indices[:, 0]],
+                         axis=1)
+    np.testing.assert_array_equal(m.spring_rest_lengths, ref)
+    np.testing.assert_array_equal(M._rest_lengths(m.positions, m.spring_indices), ref)
+    b = M.grid_band(nx, ny, 0, ny, 1.3, 0.7)
+    np.testing.assert_array_equal(b.spring_rest_lengths, ref)
+
+
+@pytest.mark.parametrize("nx,ny", [(2, 2), (2, 7), (7, 2), (3, 3), (31, 17)])
+def test_grid_families_partition_the_springs(nx, ny):
+    """mesh.grid_families groups grid_springs exactly by (kind, index delta)."""
+    springs, kinds = M.grid_springs(nx, ny)
+    ids = np.arange(len(springs))
+    seen = []
+    for (kind, delta), views in zip(((0, 1), (0, nx), (1, nx + 1), (1, nx - 1), (2, 2),
+                                     (2, 2 * nx)), M.grid_families(ids, nx, ny)):
+        got = np.sort(np.concatenate([np.ravel(v) for v in views]))
+        off = springs[:, 1] - springs[:, 0]
+        want = np.nonzero((kinds == kind) & (off == delta))[0]
+        if (kind, delta) == (1, nx - 1):  # shear (c+1 -> c+nx)
+            want = np.nonzero((kinds == 1) & (off == nx - 1))[0]
+        np.testing.assert_array_equal(got, want)
+        seen.append(got)
+    assert sum(len(x) for x in seen) == len(springs)
