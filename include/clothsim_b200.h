@@ -67,13 +67,14 @@ extern "C" {
 #define CS_FLAG_SPLIT_NORMALS 512u  /* grid path: a stand-alone normals kernel
                                        after each frame instead of fusing the
                                        previous frame's normals into the step */
-#define CS_FLAG_FUSE_NORMALS 1024u  /* grid path: always fuse (default: fused
-                                       up to 2M nodes, split above) */
+#define CS_FLAG_FUSE_NORMALS 1024u  /* grid path: fuse (the default at every
+                                       size; kept for explicitness) */
 #define CS_FLAG_THREAD_NARROW 256u  /* collision narrow phase: one thread per
                                        query instead of one warp per query */
-#define CS_FLAG_PAIRED 128u         /* fast mode: the experimental paired-column
-                                       f32x2 warp-strip kernel (cs_strip2.cu)
-                                       instead of the scalar one */
+#define CS_FLAG_PAIRED 128u         /* fast mode: the paired-column f32x2
+                                       warp-strip kernel (cs_pair3.cu, the
+                                       production path; Engine kernel="pair")
+                                       instead of the scalar strip kernel */
 
 typedef struct cs_engine cs_engine;
 
@@ -201,7 +202,12 @@ int cs_state_plane(cs_engine *h, int32_t which, void **dev_ptr, int64_t *pitch);
    peer stores over NVLink -- then signals `remote_flag` (the neighbour's flag
    word 0 if I am its upper neighbour, 1 if its lower one).  Before each force
    pass an engine's stream waits until every neighbour finished the previous
-   pass.  Link before the first frame; every band must step in lockstep. */
+   pass.  Link before the first frame; every band must step in lockstep.
+   With an obstacle (replicated per band) a frame has three handshakes:
+   post-step rows -> detect -> "detect done" -> respond -> post-respond rows.
+   Drive each band from its own CUDA context (one process per GPU): inside
+   one context a stream blocked on a flag that another stream of the same
+   context has not written yet can stall the whole context. */
 typedef struct cs_halo_peer {
     void *state[2];        /* the neighbour's state buffers (cs_state_buffers) */
     int64_t plane;         /* the neighbour's plane stride in elements */

@@ -27,7 +27,10 @@ Because each node's force sums the same springs in the same program order
 whatever band it sits in, a banded run is bit-identical to the single-GPU
 run (tests/test_bands_gloo.py checks the exchange plans on CPU; the GPU
 tests link several bands in one process).  The obstacle (if any) would be
-replicated per rank; collision across band seams is not implemented yet.
+replicated per rank.  Every band detects over its local sheet (owned rows +
+halo), but accumulates contacts only into its owned nodes and counts a hit
+only when the primitive's minimum node is owned, so positions stay
+bit-identical and the bands' hit counts sum to one engine's.
 """
 
 from __future__ import annotations
@@ -141,9 +144,12 @@ class BandedEngine:
 
     def __init__(self, nx, ny, params, rank, world, group=None, stream=None, width=1.0,
                  height=1.0, node_mass=0.05, pinned_rows="first", exchange="nccl",
-                 precision="fast", **engine_kw):
-        from .engine import Engine
-        from .mesh import grid_band
+                 precision="fast", mesh=None, obstacle=None, **engine_kw):
+        """A band of the hanging nx x ny cloth (BASELINE config 5), or -- with
+        `mesh` -- of any grid ClothMesh (e.g. a drop scene) with the static
+        `obstacle` replicated on every band."""
+        from .engine import Engine, _grid_stencil_rest
+        from .mesh import band_of_mesh, grid_band
 
         if exchange not in ("nccl", "p2p"):
             raise ValueError("exchange must be 'nccl' or 'p2p'")
@@ -152,14 +158,21 @@ class BandedEngine:
         self._opened = []
         self.plan = HaloPlan(ny, world, rank)
         self.nx, self.ny = nx, ny
-        mesh = grid_band(nx, ny, self.plan.l0, self.plan.l1, width, height,
-                         total_mass=node_mass * nx * ny, pinned_rows=pinned_rows)
-        rot = np.zeros_like(mesh.positions)  # scenes._rotate_xz_to_xy
-        rot[:, 0] = mesh.positions[:, 0]
-        rot[:, 1] = -mesh.positions[:, 2]
-        mesh.positions = rot
-        self.mesh = mesh
-        self.engine = Engine(mesh, params=params, stream=stream, precision=precision, **engine_kw)
+        if mesh is not None:
+            stencil = _grid_stencil_rest(mesh)
+            if stencil is None or (stencil[0], stencil[1]) != (nx, ny):
+                raise ValueError("row bands need an nx x ny grid mesh with uniform spring families")
+            band = band_of_mesh(mesh, nx, ny, stencil[2], self.plan.l0, self.plan.l1)
+        else:
+            band = grid_band(nx, ny, self.plan.l0, self.plan.l1, width, height,
+                             total_mass=node_mass * nx * ny, pinned_rows=pinned_rows)
+            rot = np.zeros_like(band.positions)  # scenes._rotate_xz_to_xy
+            rot[:, 0] = band.positions[:, 0]
+            rot[:, 1] = -band.positions[:, 2]
+            band.positions = rot
+        self.mesh = band
+        self.engine = Engine(band, obstacle, params=params, stream=stream, precision=precision,
+                             **engine_kw)
         self.group = group
         self.local_rows = self.plan.l1 - self.plan.l0
 

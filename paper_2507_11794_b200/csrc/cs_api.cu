@@ -152,6 +152,8 @@ struct cs_engine {
         A.pad = 1e-5f;  // kernels.py:48 BOX_PAD
         A.scale_f = sp.scale_f;
         A.scale_d = sp.scale_d;
+        A.own_lo = banded ? (int64_t)sp.row_lo * pitch : 0;
+        A.own_hi = banded ? (int64_t)sp.row_hi * pitch : INT64_MAX;
         return A;
     }
     int kernels_per_frame() const {
@@ -403,6 +405,29 @@ static int banded_frame(cs_engine *h) {
         }
         CK(cudaGetLastError());
         h->cur = dst;
+        if (int r = halo_signal(h)) return r;
+    }
+    if (h->has_obstacle) {
+        // Detection needs the neighbours' post-step boundary rows (the halo
+        // now holds them), and the respond pass changes owned nodes after
+        // they were sent -- so: wait, detect, signal "detect done", respond,
+        // wait until the neighbours finished detecting (they read the halo
+        // we are about to overwrite), push the post-respond boundary rows,
+        // signal.  Each band accumulates only into its owned nodes and
+        // counts only the hits of primitives whose minimum node it owns.
+        if (int r = halo_wait(h)) return r;
+        pass_detect(h);
+        if (int r = halo_signal(h)) return r;
+        pass_respond(h);
+        if (int r = halo_wait(h)) return r;
+        const HaloDst hd = halo_dst(h, h->cur);
+        if (h->up.on)
+            launch_push_rows((const float *)h->state[h->cur], h->plane, (int)h->pitch,
+                             (int)h->up.src_row0, (int)(h->up.src_row0 + h->up.rows), hd.up, h->st);
+        if (h->dn.on)
+            launch_push_rows((const float *)h->state[h->cur], h->plane, (int)h->pitch,
+                             (int)h->dn.src_row0, (int)(h->dn.src_row0 + h->dn.rows), hd.dn, h->st);
+        CK(cudaGetLastError());
         if (int r = halo_signal(h)) return r;
     }
     h->forces_valid = true;
@@ -1092,7 +1117,6 @@ extern "C" int cs_set_halo_peers(cs_engine *h, int64_t row_lo, int64_t row_hi,
     if (!h) return fail(CS_E_INVALID, "null engine");
     if (!h->grid || !h->strip || h->fp64)
         return fail(CS_E_INVALID, "row bands need the float32 grid strip path");
-    if (h->has_obstacle) return fail(CS_E_INVALID, "collision across row bands is not supported");
     if (h->frames != 0 || h->cur != 0)
         return fail(CS_E_INVALID, "link row bands before the first frame (lockstep parity)");
     if (row_lo < 0 || row_hi > h->rows || row_lo >= row_hi)

@@ -386,6 +386,7 @@ __device__ __forceinline__ float np_max(float a, float b) {
 // node's count went 0 -> 1 (it joins the touched list).
 __device__ __forceinline__ void accumulate(const CollideArgs &A, int64_t g, const float *p,
                                            const float *hit, const float *on, uint32_t tri) {
+    if (g < A.own_lo || g >= A.own_hi) return;  // another band's node
     if (A.clog) {  // optional (node, triangle) contact log for the parity tests
         const uint32_t slot = atomicAdd(A.clog_n, 1u);
         if (slot < A.clog_cap) {
@@ -405,6 +406,10 @@ __device__ __forceinline__ void accumulate(const CollideArgs &A, int64_t g, cons
         const uint32_t slot = atomicAdd(A.touched_n, 1u);
         A.touched[slot] = (uint32_t)g;
     }
+}
+
+__device__ __forceinline__ uint32_t owned_hit(const CollideArgs &A, int64_t min_node) {
+    return (min_node >= A.own_lo) & (min_node < A.own_hi);
 }
 
 __device__ __forceinline__ void load_pos(const CollideArgs &A, int64_t g, float *p) {
@@ -466,7 +471,7 @@ k_detect_cloth_edges(const CollideArgs A, const GridDesc g, const uint32_t *__re
                                 continue;
                             float pt[3];
                             if (!seg_tri(st, en, c, c + 3, c + 6, A.eps, pt)) continue;
-                            ++hits;
+                            hits += owned_hit(A, ga < gb ? ga : gb);
                             const float *nrm = normals + 3 * (int64_t)t;
                             const float sa = dot3x(fsub(st[0], pt[0]), fsub(st[1], pt[1]),
                                                    fsub(st[2], pt[2]), nrm[0], nrm[1], nrm[2]);
@@ -541,7 +546,7 @@ k_detect_obstacle_edges(const CollideArgs A, const GridDesc g, const uint32_t *_
                                 if (!box_overlap(elo, ehi, clo, chi)) continue;
                                 float pt[3];
                                 if (!seg_tri(st, en, v0, v1, v2, A.eps, pt)) continue;
-                                ++hits;
+                                hits += owned_hit(A, min(n0, min(n1, n2)));
                                 const float t0 = dot3x(fsub(v0[0], pt[0]), fsub(v0[1], pt[1]),
                                                        fsub(v0[2], pt[2]), nrm[0], nrm[1], nrm[2]);
                                 const float t1 = dot3x(fsub(v1[0], pt[0]), fsub(v1[1], pt[1]),
@@ -710,7 +715,7 @@ k_detect_warp(const CollideArgs A, const GridDesc g, const uint32_t *__restrict_
                     if (PASS == 0) {
                         float pt[3];
                         if (!seg_tri(v[0], v[1], cr, cr + 3, cr + 6, A.eps, pt)) continue;
-                        ++hits;
+                        hits += owned_hit(A, nid[0] < nid[1] ? nid[0] : nid[1]);
                         const float sa = dot3x(fsub(v[0][0], pt[0]), fsub(v[0][1], pt[1]),
                                                fsub(v[0][2], pt[2]), nrm[0], nrm[1], nrm[2]);
                         const float sb = dot3x(fsub(v[1][0], pt[0]), fsub(v[1][1], pt[1]),
@@ -732,7 +737,7 @@ k_detect_warp(const CollideArgs A, const GridDesc g, const uint32_t *__restrict_
                             if (!box_overlap(elo, ehi, clo, chi)) continue;
                             float pt[3];
                             if (!seg_tri(st, en, v[0], v[1], v[2], A.eps, pt)) continue;
-                            ++hits;
+                            hits += owned_hit(A, min(nid[0], min(nid[1], nid[2])));
                             const float t0s = dot3x(fsub(v[0][0], pt[0]), fsub(v[0][1], pt[1]),
                                                     fsub(v[0][2], pt[2]), nrm[0], nrm[1], nrm[2]);
                             const float t1s = dot3x(fsub(v[1][0], pt[0]), fsub(v[1][1], pt[1]),

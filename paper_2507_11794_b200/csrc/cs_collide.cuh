@@ -72,6 +72,10 @@ struct CollideArgs {
     uint32_t clog_cap;
     float eps, margin, pad, scale_f;
     double scale_d;
+    // row bands: only nodes with storage index in [own_lo, own_hi) receive
+    // contacts, and a hit counts only when its primitive's minimum node is
+    // owned -- the union over bands equals one engine
+    int64_t own_lo, own_hi;
 };
 
 // RAII device scratch for construction-time helpers

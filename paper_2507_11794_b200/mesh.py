@@ -383,6 +383,29 @@ def grid_band(nx: int, ny: int, j0: int, j1: int, width: float = 1.0, height: fl
                      triangles=grid_triangles(nx, lny))
 
 
+def band_of_mesh(mesh, nx: int, ny: int, rest6, j0: int, j1: int) -> ClothMesh:
+    """Rows [j0, j1) of an nx x ny grid ClothMesh as a stand-alone sheet for
+    a row band: the global node data of those rows, the grid topology of an
+    nx x (j1-j0) sheet, and each spring family's rest length `rest6` (the
+    global mesh's, engine._grid_stencil_rest) -- so the band's stencil
+    coefficients are the global ones bit for bit, whatever pose the scene
+    moved the cloth into after generate_cloth_grid."""
+    if not (0 <= j0 < j1 <= ny) or j1 - j0 < 2:
+        raise ValueError(f"band [{j0}, {j1}) outside a grid of {ny} rows")
+    lny = j1 - j0
+    sl = slice(j0 * nx, j1 * nx)
+    springs, kinds = grid_springs(nx, lny)
+    rest = np.empty(len(springs))
+    for value, views in zip(rest6, grid_families(rest, nx, lny)):
+        for v in views:
+            v[...] = value
+    return ClothMesh(nx=nx, ny=lny, positions=np.array(mesh.positions[sl], dtype=np.float64),
+                     masses=np.array(mesh.masses[sl], dtype=np.float64),
+                     pinned=np.array(mesh.pinned[sl], dtype=bool), spring_indices=springs,
+                     spring_rest_lengths=rest, spring_kinds=kinds,
+                     triangles=grid_triangles(nx, lny))
+
+
 def _resolve_pinned_rows(pinned_rows, ny: int):
     if pinned_rows is None or (isinstance(pinned_rows, str) and pinned_rows == "none"):
         return []

@@ -115,8 +115,12 @@ def test_c3_drapes_finite_with_contacts_in_both_modes():
 def test_p2p_bands_bit_identical_to_one_engine(world, precision, n, normals):
     """Row bands linked by peer stores inside the step kernel (the NVLink
     path of bench.py --gpus N), several bands on one device, each on its own
-    stream, ordered only by the stream flag handshake: owned rows equal the
-    single-engine run bit for bit (positions, velocities, normals)."""
+    stream: owned rows equal the single-engine run bit for bit (positions,
+    velocities, normals).  Within ONE CUDA context a stream waiting on a flag
+    that another stream of the same context has yet to write can stall the
+    context, so this single-process test enqueues one frame per band and
+    synchronises before the next (every wait is then already satisfied); the
+    cross-process tests below exercise the real blocking handshake."""
     from paper_2507_11794_b200.bands import link_local
 
     k, c = stable_coefficients(NODE_MASS, CONTACT_DT)
@@ -126,10 +130,12 @@ def test_p2p_bands_bit_identical_to_one_engine(world, precision, n, normals):
     bands = [BandedEngine(n, n, params, r, world, exchange="p2p", precision=precision,
                           normals=normals) for r in range(world)]
     link_local(bands)
-    for chunk in (1, 7, 22):  # 30 frames, enqueued band after band
-        whole.step_frames(chunk)
+    whole.step_frames(30)
+    for _ in range(30):
         for b in bands:
-            b.step(chunk)
+            b.step(1)
+        for b in bands:
+            b.engine.synchronize()
     for what in ("positions", "velocities", "normals"):
         got = np.concatenate([getattr(b, f"owned_{what}")() for b in bands])
         np.testing.assert_array_equal(got, getattr(whole, f"read_{what}")(), err_msg=what)
@@ -151,13 +157,22 @@ def test_p2p_link_validation():
         link_local(bands)
 
 
-def test_ipc_linked_bands_across_processes():
+@pytest.mark.parametrize("n,world,obstacle", [(192, 2, None), (48, 2, "icosphere:3"),
+                                              (60, 3, "uvsphere:40x40")])
+def test_ipc_linked_bands_across_processes(n, world, obstacle):
     """The multi-process link (CUDA IPC handles swapped over torch.distributed,
-    as bench.py --gpus N does across GPUs), two processes on one device."""
+    as bench.py --gpus N does across GPUs), one process per band on one
+    device, blocking flag handshake included.  With a replicated obstacle
+    (collision across band seams) the owned rows stay
+    bit-identical to one engine through contact and the bands' hit counts
+    sum to its count."""
+    import os
     import subprocess
     import sys
 
-    root = __import__("os").path.dirname(__import__("os").path.dirname(__file__))
-    res = subprocess.run([sys.executable, "tools/ipc_bands_smoke.py", "192", "2"], cwd=root,
-                         capture_output=True, text=True, timeout=280)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "tools/ipc_bands_smoke.py", str(n), str(world)]
+    if obstacle:
+        cmd.append(obstacle)
+    res = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=280)
     assert res.returncode == 0 and "'ok'" in res.stdout, res.stdout + res.stderr[-2000:]
