@@ -192,7 +192,7 @@ def main():
     if multi:
         from paper_2507_11794_b200.bands import run_banded_bench
 
-        return run_banded_bench(args, METRIC)
+        return run_banded_bench(args, METRIC, clock_sampler=ClockSampler, peak=_peaks()[0])
     scene = P.baseline_scene(config_name)
 
     import torch

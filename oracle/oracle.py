@@ -87,7 +87,13 @@ def set_threads(n: int) -> None:
 
 
 def max_threads() -> int:
-    return int(lib().or_max_threads())
+    """Host cores available to this process (not OMP_NUM_THREADS, which
+    torchrun pins to 1): the reference arm uses every core it may."""
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        cores = os.cpu_count() or 1
+    return max(cores, int(lib().or_max_threads()))
 
 
 def _p(a):

@@ -304,43 +304,82 @@ def link_local(bands):
         b.link(up, down)
 
 
-def run_banded_bench(args, metric):
+def run_banded_bench(args, metric, clock_sampler=None, peak=None):
     """bench.py for N > 1 (torchrun): config 5 split in row bands, one per GPU;
-    value = whole-job steps/s, timed with CUDA events, max over ranks."""
+    value = whole-job steps/s, timed with CUDA events, max over ranks; e2e =
+    the same through Engine.write_* + Engine.simulate with host buffers."""
+    import contextlib
+
     import torch
     import torch.distributed as dist
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from .scenes import CONTACT_DT, NODE_MASS, stable_coefficients
+    exchange = os.environ.get("CLOTHSIM_BAND_EXCHANGE", "p2p")
+    # one GPU per rank; with fewer devices than ranks (a functional run on a
+    # single-GPU box) ranks share devices -- each rank is its own process and
+    # CUDA context, which the flag handshake requires
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    if exchange == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    else:  # the data path is peer stores: the process group only swaps IPC handles
+        dist.init_process_group("gloo")
+    red_dev = "cuda" if exchange == "nccl" else "cpu"
+    from .engine import pinned_empty
     from .mesh import SimParams
+    from .scenes import CONTACT_DT, NODE_MASS, stable_coefficients
 
     n = 4096
     k, c = stable_coefficients(NODE_MASS, CONTACT_DT)
     params = SimParams(dt=CONTACT_DT, stiffness=k, damping=c)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    exchange = os.environ.get("CLOTHSIM_BAND_EXCHANGE", "p2p")
     band = BandedEngine(n, n, params, rank, world, stream=stream.cuda_stream, exchange=exchange)
     if exchange == "p2p":
         band.link_ipc()
     band.step(args.warmup)
     torch.cuda.synchronize()
     dist.barrier()
-    a = torch.cuda.Event(enable_timing=True)
-    b = torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    band.step(args.steps)
-    b.record(stream)
-    torch.cuda.synchronize()
+    sampler = clock_sampler(dev) if (clock_sampler and rank == 0) else contextlib.nullcontext()
+    with sampler as clk:
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        band.step(args.steps)
+        b.record(stream)
+        torch.cuda.synchronize()
     dist.barrier()
     finite = bool(np.isfinite(band.owned_positions()).all())
-    ms = torch.tensor([a.elapsed_time(b) / args.steps], device="cuda")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
+
+    def max_over_ranks(v):
+        t = torch.tensor([v], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms = max_over_ranks(a.elapsed_time(b) / args.steps)
+
+    # end to end with host buffers: upload this band's state from pinned
+    # memory, then Engine.simulate streams every frame's positions back
+    nloc = band.mesh.num_nodes
+    k_e2e = max(3, min(args.steps, 10))
+    host_pos = pinned_empty((nloc, 3))
+    host_vel = pinned_empty((nloc, 3))
+    host_pos[...] = band.engine.read_positions()
+    host_vel[...] = band.engine.read_velocities()
+    traj = pinned_empty((k_e2e, nloc, 3))
+    dist.barrier()
+    t0 = time.perf_counter()
+    band.engine.write_positions(host_pos)
+    band.engine.write_velocities(host_vel)
+    band.engine.simulate(k_e2e, out=traj)
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    del traj
+
+    owned = (band.plan.j1 - band.plan.j0) * n
+    frame_bytes = 60 * owned  # fused k_pair3: 24 B read + 24 B + 12 B normals written per node
+    achieved = frame_bytes / (ms * 1e-3) / 1e9  # rank 0's band kernel (all ranks equal size)
     if rank == 0:
         line = {
             "metric": metric, "value": 1000.0 / ms, "unit": "steps/s", "n_gpus": world,
@@ -355,9 +394,24 @@ def run_banded_bench(args, metric):
                                          "torch.distributed NCCL send/recv after each step"),
                        "l2": "inputs (16.8M nodes, 805 MB/step) larger than L2"},
             "node_updates_per_s": 1000.0 / ms * n * n,
-            "gpu_launches": args.steps * band.engine.kernels_per_frame,
+            "roofline": {"bound": "hbm", "kernel": "k_pair3<NORMALS=1> on rank 0's band",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak if peak else None, "traffic": None,
+                         "bytes_per_launch": frame_bytes, "bytes_per_node": 60,
+                         "launch_ms": ms},
+            "e2e": {"value": k_e2e / e2e_s, "unit": "steps/s",
+                    "h2d_bytes_per_step": int(24 * n * n / k_e2e), "d2h_bytes_per_step": 12 * n * n,
+                    "api": "Engine.write_positions/write_velocities + Engine.simulate per band",
+                    "frames": k_e2e},
+            "gpu_launches": args.steps * band.engine.kernels_per_frame * world,
             "finite": finite,
+            "devices": torch.cuda.device_count(),
         }
+        if clock_sampler:
+            line["clocks"] = clk.summary()
+        if torch.cuda.device_count() < world:
+            line["note"] = (f"{world} ranks shared {torch.cuda.device_count()} GPU(s): a "
+                            "functional run, not a scaling measurement")
         print(json.dumps(line))
     if exchange == "p2p":
         band.close()
