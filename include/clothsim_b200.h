@@ -70,7 +70,10 @@ extern "C" {
 #define CS_FLAG_FUSE_NORMALS 1024u  /* grid path: fuse (the default at every
                                        size; kept for explicitness) */
 #define CS_FLAG_THREAD_NARROW 256u  /* collision narrow phase: one thread per
-                                       query instead of one warp per query */
+                                       query (default: 32-query batches per
+                                       warp, flattened over cells/candidates) */
+#define CS_FLAG_WARP_NARROW 2048u   /* collision narrow phase: one warp per
+                                       query */
 #define CS_FLAG_PAIRED 128u         /* fast mode: the paired-column f32x2
                                        warp-strip kernel (cs_pair3.cu, the
                                        production path; Engine kernel="pair")

@@ -694,7 +694,8 @@ static int build(cs_engine *h, const cs_desc *d) {
         if (build_broadphase(h->bp, h->corners, h->nt, d->obstacle_corners, d->cell_size, h->st))
             return fail(CS_E_CUDA, std::string("broad-phase build failed: ") +
                                        cudaGetErrorString(cudaGetLastError()));
-        h->bp.warp_per_query = (d->flags & CS_FLAG_THREAD_NARROW) ? 0 : 1;
+        h->bp.warp_per_query = (d->flags & CS_FLAG_THREAD_NARROW) ? 0
+                               : (d->flags & CS_FLAG_WARP_NARROW) ? 1 : 2;
     }
     CK(cudaStreamSynchronize(h->st));
     CK(cudaGetLastError());

@@ -758,6 +758,240 @@ k_detect_warp(const CollideArgs A, const GridDesc g, const uint32_t *__restrict_
     count_hits(A.frame_hits, hits);
 }
 
+// ---------------------------------------------------------------------------
+// Batched narrow phase (default): a warp takes 32 QUERIES, one per lane, and
+// flattens all of their (query, grid cell) pairs and then all of those
+// cells' candidate triangles across the 32 lanes -- "one warp per
+// cell-candidate batch".  The warp-per-query kernel above leaves most lanes
+// idle (a draped cloth edge meets ~5-20 candidates); here every lane of
+// every inner iteration tests a real (query, candidate) pair, and the
+// queries' geometry sits in shared memory where any lane can read it.  Same
+// box test, dedup rule, predicate, accumulation and hit ownership as the
+// other two mappings, so the hit set and the integer accumulators are
+// identical.
+// ---------------------------------------------------------------------------
+constexpr int BATCH_WARPS = 8;
+struct QuerySlot {
+    float v[3][3];
+    float lo[3], hi[3];   // query box (PASS 0: padded segment box; PASS 1: tri box +- 2 pad)
+    float clo[3], chi[3]; // PASS 1: unpadded cloth triangle box
+    int64_t nid[3];
+    int a[3], ex, ey;     // first cell and extents of the cell range
+};
+
+__device__ __forceinline__ int warp_owner(uint32_t incl, uint32_t t) {
+    // smallest lane L with incl[L] > t (incl non-decreasing across lanes)
+    int o = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+        const uint32_t probe = __shfl_sync(0xffffffffu, incl, o + step - 1);
+        if (probe <= t) o += step;
+    }
+    return o;
+}
+
+// One narrow-phase item: query slot `qs` of this warp against obstacle
+// triangle `tri` (PASS 1: its edge `slot`).  Returns the hits it owns.
+template <int PASS>
+__device__ __forceinline__ uint32_t narrow_item(const CollideArgs &A, const QuerySlot &Q,
+                                                uint32_t tri, int slot,
+                                                const float *__restrict__ corners,
+                                                const float *__restrict__ normals) {
+    const float *cr = corners + 9 * (int64_t)tri;
+    const float *nrm = normals + 3 * (int64_t)tri;
+    float v[3][3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) v[k][d] = Q.v[k][d];
+    float pt[3];
+    if (PASS == 0) {
+        if (!seg_tri(v[0], v[1], cr, cr + 3, cr + 6, A.eps, pt)) return 0;
+        const float sa = dot3x(fsub(v[0][0], pt[0]), fsub(v[0][1], pt[1]), fsub(v[0][2], pt[2]),
+                               nrm[0], nrm[1], nrm[2]);
+        const float sb = dot3x(fsub(v[1][0], pt[0]), fsub(v[1][1], pt[1]), fsub(v[1][2], pt[2]),
+                               nrm[0], nrm[1], nrm[2]);
+        const float sign = np_max(sa, sb) >= 0.f ? 1.f : -1.f;
+        const float on[3] = {fmul(nrm[0], sign), fmul(nrm[1], sign), fmul(nrm[2], sign)};
+        accumulate(A, Q.nid[0], v[0], pt, on, tri);
+        accumulate(A, Q.nid[1], v[1], pt, on, tri);
+        return owned_hit(A, Q.nid[0] < Q.nid[1] ? Q.nid[0] : Q.nid[1]);
+    } else {
+        const float *st = cr + 3 * slot;
+        const float *en = cr + 3 * (slot == 2 ? 0 : slot + 1);
+        if (!seg_tri(st, en, v[0], v[1], v[2], A.eps, pt)) return 0;
+        const float t0s = dot3x(fsub(v[0][0], pt[0]), fsub(v[0][1], pt[1]), fsub(v[0][2], pt[2]),
+                                nrm[0], nrm[1], nrm[2]);
+        const float t1s = dot3x(fsub(v[1][0], pt[0]), fsub(v[1][1], pt[1]), fsub(v[1][2], pt[2]),
+                                nrm[0], nrm[1], nrm[2]);
+        const float t2s = dot3x(fsub(v[2][0], pt[0]), fsub(v[2][1], pt[1]), fsub(v[2][2], pt[2]),
+                                nrm[0], nrm[1], nrm[2]);
+        const float sign = fadd(fadd(t0s, t1s), t2s) >= 0.f ? 1.f : -1.f;
+        const float on[3] = {fmul(nrm[0], sign), fmul(nrm[1], sign), fmul(nrm[2], sign)};
+        accumulate(A, Q.nid[0], v[0], pt, on, tri);
+        accumulate(A, Q.nid[1], v[1], pt, on, tri);
+        accumulate(A, Q.nid[2], v[2], pt, on, tri);
+        return owned_hit(A, min(Q.nid[0], min(Q.nid[1], Q.nid[2])));
+    }
+}
+
+constexpr int QCAP = 128;  // per-warp item queue: < 32 left + 32 lanes x 3 slots
+
+template <int PASS>
+__global__ void __launch_bounds__(32 * BATCH_WARPS)
+k_detect_batch(const CollideArgs A, const GridDesc g, const uint32_t *__restrict__ cbeg,
+               const uint32_t *__restrict__ cend, const uint32_t *__restrict__ ctri,
+               const float *__restrict__ tbox, const float *__restrict__ corners,
+               const float *__restrict__ normals, const int32_t *__restrict__ items, int64_t nq,
+               int qb) {
+    __shared__ QuerySlot slots[BATCH_WARPS][32];
+    // items that survived the box / dedup (/ edge box) filters wait here until
+    // a full warp's worth can run the predicate with every lane active
+    __shared__ uint32_t qtri[BATCH_WARPS][QCAP];
+    __shared__ uint8_t qmeta[BATCH_WARPS][QCAP];  // query slot << 2 | edge slot
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    // qb queries per warp (lanes >= qb hold none): 32 when queries are
+    // plentiful, fewer so that small clouds still spread over every SM
+    const int64_t q = (blockIdx.x * (int64_t)BATCH_WARPS + w) * qb + lane;
+    QuerySlot &my = slots[w][lane];
+    const int nv = PASS == 0 ? 2 : 3;
+    uint32_t ncell = 0;
+    if (lane < qb && q < nq) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if (k < nv) {
+                my.nid[k] = items[nv * q + k];
+                load_pos(A, my.nid[k], my.v[k]);
+            }
+        }
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            if (PASS == 0) {  // kernels.py:55-59: padded segment box
+                my.lo[d] = fsub(fminf(my.v[0][d], my.v[1][d]), A.pad);
+                my.hi[d] = fadd(fmaxf(my.v[0][d], my.v[1][d]), A.pad);
+            } else {          // cloth triangle box, queried padded by 2*pad
+                my.clo[d] = fminf(fminf(my.v[0][d], my.v[1][d]), my.v[2][d]);
+                my.chi[d] = fmaxf(fmaxf(my.v[0][d], my.v[1][d]), my.v[2][d]);
+                my.lo[d] = my.clo[d] - 2.0f * A.pad;
+                my.hi[d] = my.chi[d] + 2.0f * A.pad;
+            }
+        }
+        if (g.overlaps(my.lo, my.hi)) {
+            int a[3], b[3];
+            g.cell_range(my.lo, my.hi, a, b);
+            my.a[0] = a[0];
+            my.a[1] = a[1];
+            my.a[2] = a[2];
+            my.ex = b[0] - a[0] + 1;
+            my.ey = b[1] - a[1] + 1;
+            ncell = (uint32_t)(my.ex * my.ey * (b[2] - a[2] + 1));
+        }
+    }
+    __syncwarp();
+    uint32_t hits = 0;
+    int qn = 0;  // queued items (warp-uniform)
+    auto drain = [&](int keep) {  // run the predicate on full warps of queued items
+        while (qn > keep) {
+            const int take = qn - keep < 32 ? qn - keep : 32;
+            __syncwarp();
+            if (lane < take) {
+                const int k = qn - take + lane;
+                const uint8_t meta = qmeta[w][k];
+                hits += narrow_item<PASS>(A, slots[w][meta >> 2], qtri[w][k], meta & 3, corners,
+                                          normals);
+            }
+            qn -= take;
+            __syncwarp();
+        }
+    };
+    auto push = [&](bool want, uint32_t tri, int qs, int slot) {
+        const uint32_t m = __ballot_sync(0xffffffffu, want);
+        if (want) {
+            const int k = qn + __popc(m & lt_mask);
+            qtri[w][k] = tri;
+            qmeta[w][k] = (uint8_t)((qs << 2) | slot);
+        }
+        qn += __popc(m);
+    };
+    const uint32_t cincl = warp_incl_scan(ncell);
+    const uint32_t ctotal = __shfl_sync(0xffffffffu, cincl, 31);
+    for (uint32_t c0 = 0; c0 < ctotal; c0 += 32) {
+        // this lane's (query, cell) pair
+        const uint32_t c = c0 + lane;
+        int oq = 0, cx = 0, cy = 0, cz = 0;
+        uint32_t beg = 0, cnt = 0;
+        {
+            const int o = warp_owner(cincl, c);
+            const uint32_t oincl = __shfl_sync(0xffffffffu, cincl, o);
+            const uint32_t on = __shfl_sync(0xffffffffu, ncell, o);
+            if (c < ctotal) {
+                const QuerySlot &Q = slots[w][o];
+                const int local = (int)(c - (oincl - on));
+                cx = Q.a[0] + local % Q.ex;
+                cy = Q.a[1] + (local / Q.ex) % Q.ey;
+                cz = Q.a[2] + local / (Q.ex * Q.ey);
+                const uint32_t key = g.key(cx, cy, cz);
+                beg = cbeg[key];
+                cnt = cend[key] - beg;
+                oq = o;
+            }
+        }
+        const uint32_t incl = warp_incl_scan(cnt);
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+            const uint32_t t = t0 + lane;
+            const int o = warp_owner(incl, t);
+            const uint32_t ob = __shfl_sync(0xffffffffu, beg, o);
+            const uint32_t oi = __shfl_sync(0xffffffffu, incl, o);
+            const uint32_t oc = __shfl_sync(0xffffffffu, cnt, o);
+            const int ox = __shfl_sync(0xffffffffu, cx, o);
+            const int oy = __shfl_sync(0xffffffffu, cy, o);
+            const int oz = __shfl_sync(0xffffffffu, cz, o);
+            const int qq = __shfl_sync(0xffffffffu, oq, o);
+            bool ok = t < total;
+            uint32_t tri = 0;
+            if (ok) {
+                const QuerySlot &Q = slots[w][qq];
+                tri = ctri[ob + (t - (oi - oc))];
+                const float *tb = tbox + 6 * (int64_t)tri;
+                const float tlo[3] = {tb[0], tb[1], tb[2]}, thi[3] = {tb[3], tb[4], tb[5]};
+                // box test, then dedup: the minimum corner of the intersection
+                // lies in this cell
+                ok = box_overlap(Q.lo, Q.hi, tlo, thi) &&
+                     g.cell_of(fmaxf(Q.lo[0], tlo[0]), 0) == ox &&
+                     g.cell_of(fmaxf(Q.lo[1], tlo[1]), 1) == oy &&
+                     g.cell_of(fmaxf(Q.lo[2], tlo[2]), 2) == oz;
+            }
+            if (PASS == 0) {
+                push(ok, tri, qq, 0);
+            } else {
+                const float *cr = corners + 9 * (int64_t)tri;
+#pragma unroll
+                for (int slot = 0; slot < 3; ++slot) {  // obstacle edge 3t+slot
+                    bool e_ok = ok;
+                    if (e_ok) {
+                        const QuerySlot &Q = slots[w][qq];
+                        const float *st = cr + 3 * slot;
+                        const float *en = cr + 3 * (slot == 2 ? 0 : slot + 1);
+                        float elo[3], ehi[3];
+#pragma unroll
+                        for (int d = 0; d < 3; ++d) {
+                            elo[d] = fsub(fminf(st[d], en[d]), A.pad);
+                            ehi[d] = fadd(fmaxf(st[d], en[d]), A.pad);
+                        }
+                        e_ok = box_overlap(elo, ehi, Q.clo, Q.chi);
+                    }
+                    push(e_ok, tri, qq, slot);
+                }
+            }
+            drain(31);
+        }
+    }
+    drain(0);
+    count_hits(A.frame_hits, hits);
+}
+
 __global__ void k_tri_boxes(int64_t nt, const float *__restrict__ corners, float *__restrict__ box) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= nt) return;
@@ -776,6 +1010,31 @@ void launch_tri_boxes(int64_t nt, const float *corners, float *box, cudaStream_t
 void launch_detect(const CollideArgs &A, const BroadPhase &bp, const float *corners,
                    const float *normals, const int32_t *edges, int64_t ne, const int32_t *tris,
                    int64_t nc, cudaStream_t st) {
+    if (bp.warp_per_query == 2) {
+        // queries per warp: the largest power of two <= 32 that still leaves
+        // >= ~48 warps per SM (148 SMs) -- batches for big clouds (C3), one
+        // query per warp for small ones (C4)
+        auto qb_for = [](int64_t nq) {
+            int qb = 32;
+            while (qb > 1 && nq / qb < (int64_t)148 * 48) qb >>= 1;
+            return qb;
+        };
+        if (ne > 0) {
+            const int qb = qb_for(ne);
+            const int64_t warps = (ne + qb - 1) / qb;
+            k_detect_batch<0><<<nblk(warps, BATCH_WARPS), 32 * BATCH_WARPS, 0, st>>>(
+                A, bp.grid, bp.cell_begin, bp.cell_end, bp.cell_tris, bp.tri_box, corners, normals,
+                edges, ne, qb);
+        }
+        if (nc > 0) {
+            const int qb = qb_for(nc);
+            const int64_t warps = (nc + qb - 1) / qb;
+            k_detect_batch<1><<<nblk(warps, BATCH_WARPS), 32 * BATCH_WARPS, 0, st>>>(
+                A, bp.grid, bp.cell_begin, bp.cell_end, bp.cell_tris, bp.tri_box, corners, normals,
+                tris, nc, qb);
+        }
+        return;
+    }
     if (bp.warp_per_query) {
         if (ne > 0)
             k_detect_warp<0><<<nblk(ne * 32, 256), 256, 0, st>>>(A, bp.grid, bp.cell_begin, bp.cell_end,

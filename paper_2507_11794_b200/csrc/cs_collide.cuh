@@ -51,7 +51,8 @@ struct BroadPhase {
     uint32_t *cell_keys = nullptr;   // sorted (cell key) per reference
     uint32_t *cell_tris = nullptr;   // triangle id per reference
     float *tri_box = nullptr;        // per triangle: lo xyz, hi xyz (kernels.py:62-66)
-    int warp_per_query = 1;          // narrow phase: warp per query (1) or thread (0)
+    int warp_per_query = 2;          // narrow phase: 32-query batches per warp (2),
+                                     // warp per query (1) or thread per query (0)
 };
 
 struct CollideArgs {

@@ -137,7 +137,7 @@ def test_grid_kernels_agree_with_csr(shape):
                 np.testing.assert_allclose(e.read_normals(), ref.read_normals(), atol=1e-5)
 
 
-@pytest.mark.parametrize("narrow", ["warp", "thread"])
+@pytest.mark.parametrize("narrow", ["batch", "warp", "thread"])
 @pytest.mark.parametrize("cell", [None, 0.02, 0.003])
 def test_narrow_phase_mappings_and_cell_sizes_are_bit_identical(narrow, cell):
     """The hit set may not depend on how candidates are found."""
