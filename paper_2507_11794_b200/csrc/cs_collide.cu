@@ -252,6 +252,22 @@ static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / 
 
 void launch_tri_boxes(int64_t nt, const float *corners, float *box, cudaStream_t st);
 
+__global__ void k_pack_cells(int64_t n, const uint32_t *__restrict__ beg,
+                             const uint32_t *__restrict__ end, uint2 *__restrict__ be) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) be[i] = make_uint2(beg[i], end[i]);
+}
+
+__global__ void k_ref_boxes(int64_t n, const uint32_t *__restrict__ tris,
+                            const float *__restrict__ tbox, float4 *__restrict__ out) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const uint32_t t = tris[r];
+    const float *b = tbox + 6 * (int64_t)t;
+    out[2 * r] = make_float4(b[0], b[1], b[2], __uint_as_float(t));
+    out[2 * r + 1] = make_float4(b[3], b[4], b[5], 0.f);
+}
+
 int build_broadphase(BroadPhase &bp, const float *d_corners, int64_t nt, const float *h_corners,
                      float cell_size, cudaStream_t st) {
     // grid over the obstacle's bounding box (host: static data, computed once)
@@ -328,11 +344,19 @@ int build_broadphase(BroadPhase &bp, const float *d_corners, int64_t nt, const f
     cudaFree(tk);
     cudaMalloc(&bp.tri_box, 6 * (nt > 0 ? nt : 1) * sizeof(float));
     launch_tri_boxes(nt, d_corners, bp.tri_box, st);
+    cudaMalloc(&bp.cell_be, bp.num_cells * sizeof(uint2));
+    cudaMalloc(&bp.ref_box, 2 * (total + 1) * sizeof(float4));
+    k_pack_cells<<<nblk(bp.num_cells, 256), 256, 0, st>>>(bp.num_cells, bp.cell_begin, bp.cell_end,
+                                                          bp.cell_be);
+    if (total > 0)
+        k_ref_boxes<<<nblk(total, 256), 256, 0, st>>>(total, bp.cell_tris, bp.tri_box, bp.ref_box);
     cudaFree(tv);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 void free_broadphase(BroadPhase &bp) {
+    cudaFree(bp.cell_be);
+    cudaFree(bp.ref_box);
     cudaFree(bp.cell_begin);
     cudaFree(bp.cell_end);
     cudaFree(bp.cell_keys);
@@ -839,9 +863,8 @@ constexpr int QCAP = 128;  // per-warp item queue: < 32 left + 32 lanes x 3 slot
 
 template <int PASS>
 __global__ void __launch_bounds__(32 * BATCH_WARPS)
-k_detect_batch(const CollideArgs A, const GridDesc g, const uint32_t *__restrict__ cbeg,
-               const uint32_t *__restrict__ cend, const uint32_t *__restrict__ ctri,
-               const float *__restrict__ tbox, const float *__restrict__ corners,
+k_detect_batch(const CollideArgs A, const GridDesc g, const uint2 *__restrict__ cbe,
+               const float4 *__restrict__ rbox, const float *__restrict__ corners,
                const float *__restrict__ normals, const int32_t *__restrict__ items, int64_t nq,
                int qb) {
     __shared__ QuerySlot slots[BATCH_WARPS][32];
@@ -931,9 +954,9 @@ k_detect_batch(const CollideArgs A, const GridDesc g, const uint32_t *__restrict
                 cx = Q.a[0] + local % Q.ex;
                 cy = Q.a[1] + (local / Q.ex) % Q.ey;
                 cz = Q.a[2] + local / (Q.ex * Q.ey);
-                const uint32_t key = g.key(cx, cy, cz);
-                beg = cbeg[key];
-                cnt = cend[key] - beg;
+                const uint2 r = cbe[g.key(cx, cy, cz)];
+                beg = r.x;
+                cnt = r.y - r.x;
                 oq = o;
             }
         }
@@ -953,9 +976,10 @@ k_detect_batch(const CollideArgs A, const GridDesc g, const uint32_t *__restrict
             uint32_t tri = 0;
             if (ok) {
                 const QuerySlot &Q = slots[w][qq];
-                tri = ctri[ob + (t - (oi - oc))];
-                const float *tb = tbox + 6 * (int64_t)tri;
-                const float tlo[3] = {tb[0], tb[1], tb[2]}, thi[3] = {tb[3], tb[4], tb[5]};
+                const int64_t ref = ob + (t - (oi - oc));
+                const float4 b0 = rbox[2 * ref], b1 = rbox[2 * ref + 1];
+                tri = __float_as_uint(b0.w);
+                const float tlo[3] = {b0.x, b0.y, b0.z}, thi[3] = {b1.x, b1.y, b1.z};
                 // box test, then dedup: the minimum corner of the intersection
                 // lies in this cell
                 ok = box_overlap(Q.lo, Q.hi, tlo, thi) &&
@@ -1023,15 +1047,13 @@ void launch_detect(const CollideArgs &A, const BroadPhase &bp, const float *corn
             const int qb = qb_for(ne);
             const int64_t warps = (ne + qb - 1) / qb;
             k_detect_batch<0><<<nblk(warps, BATCH_WARPS), 32 * BATCH_WARPS, 0, st>>>(
-                A, bp.grid, bp.cell_begin, bp.cell_end, bp.cell_tris, bp.tri_box, corners, normals,
-                edges, ne, qb);
+                A, bp.grid, bp.cell_be, bp.ref_box, corners, normals, edges, ne, qb);
         }
         if (nc > 0) {
             const int qb = qb_for(nc);
             const int64_t warps = (nc + qb - 1) / qb;
             k_detect_batch<1><<<nblk(warps, BATCH_WARPS), 32 * BATCH_WARPS, 0, st>>>(
-                A, bp.grid, bp.cell_begin, bp.cell_end, bp.cell_tris, bp.tri_box, corners, normals,
-                tris, nc, qb);
+                A, bp.grid, bp.cell_be, bp.ref_box, corners, normals, tris, nc, qb);
         }
         return;
     }

@@ -51,6 +51,11 @@ struct BroadPhase {
     uint32_t *cell_keys = nullptr;   // sorted (cell key) per reference
     uint32_t *cell_tris = nullptr;   // triangle id per reference
     float *tri_box = nullptr;        // per triangle: lo xyz, hi xyz (kernels.py:62-66)
+    // batched narrow phase: (begin, end) per cell in one 8-byte word, and per
+    // sorted reference its triangle's box with the triangle id in lo.w --
+    // one 32-byte load per candidate instead of ctri -> tri_box
+    uint2 *cell_be = nullptr;
+    float4 *ref_box = nullptr;
     int warp_per_query = 2;          // narrow phase: 32-query batches per warp (2),
                                      // warp per query (1) or thread per query (0)
 };
