@@ -132,6 +132,13 @@ typedef struct cs_desc {
     /* CUDA stream to launch on (cudaStream_t); NULL = the library creates
        its own non-blocking stream */
     void *stream;
+    /* CS_FLAG_FP64 with an obstacle: (T,3,3) f64 corners and (T,3) f64 unit
+       face normals, and the float64 epsilon_mt / response_margin, for the
+       solver-exact collision (collision.py:243-346) */
+    const double *obstacle_corners64;
+    const double *obstacle_normals64;
+    double epsilon_mt64;
+    double response_margin64;
 } cs_desc;
 
 typedef struct cs_stats {

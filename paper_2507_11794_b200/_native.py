@@ -78,6 +78,10 @@ class CsDesc(ctypes.Structure):
         ("substeps", ctypes.c_int32),
         ("cell_size", ctypes.c_float),
         ("stream", _P),
+        ("obstacle_corners64", _P),
+        ("obstacle_normals64", _P),
+        ("epsilon_mt64", ctypes.c_double),
+        ("response_margin64", ctypes.c_double),
     ]
 
 

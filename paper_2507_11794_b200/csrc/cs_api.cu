@@ -19,6 +19,7 @@
 
 #include "../../include/clothsim_b200.h"
 #include "cs_collide.cuh"
+#include "cs_collide64.cuh"
 #include "cs_common.cuh"
 #include "cs_kernels.cuh"
 
@@ -97,6 +98,11 @@ struct cs_engine {
     bool normals_stale = false; // normals buffer holds the previous frame's (fused)
     float *corners = nullptr, *onormals = nullptr;
     BroadPhase bp;
+    // float64 solver-exact collision (cs_collide64.cu)
+    double *corners64 = nullptr, *onormals64 = nullptr;
+    double eps64 = 1e-6, margin64 = 1e-3;
+    Contacts64 c64;
+    uint32_t c64_n = 0;
     int32_t *acc = nullptr, *count = nullptr;
     uint32_t *touched = nullptr, *touched_n = nullptr;
     // [frame_hits, frame_responded, hit_counter, frame_counter, ring (2 x kRing)]
@@ -264,16 +270,53 @@ static void pass_force_integrate(cs_engine *h, bool fuse_normals = false) {
     h->forces_valid = true;
 }
 
+static Detect64Args detect64_args(const cs_engine *h) {
+    Detect64Args D{};
+    D.pos = (const double *)h->state[h->cur];
+    D.plane = h->plane;
+    D.corners = h->corners64;
+    D.normals = h->onormals64;
+    D.nt = h->nt;
+    D.nc = h->nc;
+    D.eps = h->eps64;
+    D.margin = h->margin64;
+    D.pad = 1e-5f;
+    return D;
+}
+
 static void pass_detect(cs_engine *h) {
     cudaMemsetAsync(h->stats, 0, 2 * sizeof(unsigned long long), h->st);
     if (h->clog) cudaMemsetAsync(h->clog_n, 0, sizeof(uint32_t), h->st);
     if (!h->has_obstacle) return;
+    if (h->fp64) {
+        // the float64 path synchronises: its contact count sizes the sort,
+        // and an overflowing pass is re-run with larger buffers
+        for (;;) {
+            launch_detect64(h->c64, detect64_args(h), h->bp, h->edges_g, h->ne, h->tris_g, h->nc,
+                            h->stats, h->st);
+            cudaMemcpyAsync(&h->c64_n, h->c64.count, sizeof(uint32_t), cudaMemcpyDeviceToHost, h->st);
+            cudaStreamSynchronize(h->st);
+            if (h->c64_n <= h->c64.cap) break;
+            h->c64.reserve(2 * (int64_t)h->c64_n);
+            cudaMemsetAsync(h->stats, 0, 2 * sizeof(unsigned long long), h->st);
+        }
+        return;
+    }
     launch_detect(h->cargs(), h->bp, h->corners, h->onormals, h->edges_g, h->ne, h->tris_g, h->nc,
                   h->st);
 }
 
 static void pass_respond(cs_engine *h) {
     if (!h->has_obstacle) return;
+    if (h->fp64) {
+        int bits = 1;
+        while (((int64_t)1 << bits) < h->N) ++bits;
+        launch_respond64(h->c64, h->c64_n, bits, (double *)h->state[h->cur], h->plane, h->pinned8,
+                         h->average ? 1 : 0, h->stats + 1, h->st);
+        h->c64_n = 0;
+        launch_respond_end(h->cargs(), true, h->st);
+        return;
+    }
     launch_respond(h->cargs(), (float *)h->state[h->cur], h->grid ? h->pinbits : nullptr,
                    h->grid ? nullptr : h->inv_mass, h->average ? 1 : 0, h->N, h->num_sms,
                    /*end_of_frame=*/true, h->st);
@@ -459,8 +502,8 @@ static int build(cs_engine *h, const cs_desc *d) {
     h->substeps = d->substeps < 1 ? 1 : d->substeps;
     h->N = N;
     if (h->fp64 && h->fixed) return fail(CS_E_INVALID, "CS_FLAG_FP64 and CS_FLAG_FIXED_POINT are exclusive");
-    if (h->fp64 && d->num_obstacle_tris > 0)
-        return fail(CS_E_INVALID, "float64 engines do not support obstacles yet");
+    if (h->fp64 && d->num_obstacle_tris > 0 && (!d->obstacle_corners64 || !d->obstacle_normals64))
+        return fail(CS_E_INVALID, "float64 engines with an obstacle need obstacle_corners64/normals64");
     if (h->fp64 && (!d->masses64 || !d->pinned || !d->spring_rest64))
         return fail(CS_E_INVALID, "float64 engines need masses64, pinned and spring_rest64");
 
@@ -696,6 +739,17 @@ static int build(cs_engine *h, const cs_desc *d) {
                                        cudaGetErrorString(cudaGetLastError()));
         h->bp.warp_per_query = (d->flags & CS_FLAG_THREAD_NARROW) ? 0
                                : (d->flags & CS_FLAG_WARP_NARROW) ? 1 : 2;
+        if (h->fp64) {
+            CK(dalloc(&h->corners64, 9 * h->nt));
+            CK(dalloc(&h->onormals64, 3 * h->nt));
+            CK(cudaMemcpy(h->corners64, d->obstacle_corners64, 9 * h->nt * 8, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(h->onormals64, d->obstacle_normals64, 3 * h->nt * 8, cudaMemcpyHostToDevice));
+            h->eps64 = d->epsilon_mt64;
+            h->margin64 = d->response_margin64;
+            if (h->c64.reserve(std::max<int64_t>(4096, 4 * N)))
+                return fail(CS_E_CAPACITY, "float64 contact buffers");
+            h->use_graph = false;  // the float64 collision passes synchronise
+        }
     }
     CK(cudaStreamSynchronize(h->st));
     CK(cudaGetLastError());
@@ -710,10 +764,12 @@ extern "C" int cs_destroy(cs_engine *h) {
                     h->pinned8, h->ext, h->forces_raw, h->csr_off, h->csr_nbr, h->csr_kind,
                     h->csr_rest, h->csr_rest64, h->inc_off, h->inc_tri, h->face, h->tris_g,
                     h->edges_g, h->corners, h->onormals, h->acc, h->count, h->touched,
-                    h->touched_n, h->stats, h->stage, h->hflags};
+                    h->touched_n, h->stats, h->stage, h->hflags, h->corners64, h->onormals64};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (h->has_obstacle) free_broadphase(h->bp);
+    h->c64.release();
+    if (h->c64.count) cudaFree(h->c64.count);
     if (h->own_stream && h->st) cudaStreamDestroy(h->st);
     if (h->copy_st) {
         cudaStreamSynchronize(h->copy_st);

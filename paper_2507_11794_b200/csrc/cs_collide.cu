@@ -1088,6 +1088,10 @@ void launch_respond(const CollideArgs &A, float *state, const uint32_t *pinbits,
     k_respond_end<<<1, 1, 0, st>>>(A, end_of_frame ? 1 : 0);
 }
 
+void launch_respond_end(const CollideArgs &A, bool end_of_frame, cudaStream_t st) {
+    k_respond_end<<<1, 1, 0, st>>>(A, end_of_frame ? 1 : 0);
+}
+
 void launch_rebuild_touched(const CollideArgs &A, int64_t rows, int64_t nx, int64_t pitch,
                             cudaStream_t st) {
     cudaMemsetAsync(A.touched_n, 0, sizeof(uint32_t), st);

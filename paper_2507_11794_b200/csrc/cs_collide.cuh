@@ -114,6 +114,7 @@ void launch_detect(const CollideArgs &A, const BroadPhase &bp, const float *corn
 void launch_respond(const CollideArgs &A, float *state, const uint32_t *pinbits,
                     const float *inv_mass, int average, int64_t max_nodes, int num_sms,
                     bool end_of_frame, cudaStream_t st);
+void launch_respond_end(const CollideArgs &A, bool end_of_frame, cudaStream_t st);
 void launch_rebuild_touched(const CollideArgs &A, int64_t rows, int64_t nx, int64_t pitch,
                             cudaStream_t st);
 

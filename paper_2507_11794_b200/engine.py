@@ -349,6 +349,11 @@ class Engine:
             d.num_obstacle_tris = n_obs
             d.obstacle_corners = _p(keep["corners"])
             d.obstacle_normals = _p(keep["onorm"])
+            if precision == "fp64":  # solver-exact float64 collision
+                keep["corners64"] = np.ascontiguousarray(corners, dtype=np.float64)
+                keep["onorm64"] = np.ascontiguousarray(obstacle.face_normals, dtype=np.float64)
+                d.obstacle_corners64 = _p(keep["corners64"])
+                d.obstacle_normals64 = _p(keep["onorm64"])
         d.dt = p.dt / p.substeps
         for q in range(3):
             d.gravity[q] = float(p.gravity[q])
@@ -356,6 +361,8 @@ class Engine:
         d.damping = float(p.damping)
         d.epsilon_mt = float(p.epsilon_mt)
         d.response_margin = float(p.response_margin)
+        d.epsilon_mt64 = float(p.epsilon_mt)
+        d.response_margin64 = float(p.response_margin)
         d.fixed_point_scale = int(p.fixed_point_scale)
         d.substeps = int(p.substeps)
         d.cell_size = float(cell_size) if cell_size else 0.0

@@ -3,7 +3,7 @@ the reference's golden vectors.
 
 * precision="fixed": bit-identical to the reference engine (every buffer,
   every hit count, every contact) -- golden fixtures + EngineOracle.
-* precision="fp64": bit-identical to the reference solver (no obstacle).
+* precision="fp64": bit-identical to the reference solver, collision included.
 * precision="fast": within the north-star tolerances of the f64 solver --
   per step |dx|,|dv| <= 1e-5 * extent from an identical state, and
   |dx| <= 1e-3 * extent after 100 steps (C1, C2 at dt 0.004).
@@ -45,15 +45,20 @@ def test_fixed_mode_is_bit_identical_to_reference_engine(name, force_csr):
     np.testing.assert_array_equal(hits, g["eng_hits"][: len(hits)])
 
 
-@pytest.mark.parametrize("name", ["traj_hang8.npz", "traj_corner16.npz", "traj_hang12x10.npz"])
+@pytest.mark.parametrize("name", TRAJ)
 def test_fp64_mode_is_bit_identical_to_reference_solver(name):
+    """float64 engine == solver.step, including detect_all + the response
+    (drop / pull / flags scenes: contacts summed in the solver's serial
+    order), per-frame hit counts included."""
     g, eng = _run_golden(name, "fp64")
     cps = set(g["checkpoints"].tolist())
+    hits = []
     for f in range(1, max(cps) + 1):
-        eng.step()
+        hits.append(eng.step().hits)
         if f in cps:
             np.testing.assert_array_equal(eng.read_positions64(), g[f"sol_pos_{f}"])
             np.testing.assert_array_equal(eng.read_velocities64(), g[f"sol_vel_{f}"])
+    np.testing.assert_array_equal(hits, g["sol_hits"][: len(hits)])
 
 
 def _extent(mesh):
