@@ -196,6 +196,8 @@ int cs_write(cs_engine *h, int32_t buffer_id, const void *host_src);
 /* Single node accumulator write (engine.py:354-358 inject_response). */
 int cs_inject_response(cs_engine *h, int64_t node, const int32_t raw[3], int32_t count);
 int cs_synchronize(cs_engine *h);
+/* The engine's CUDA stream (cudaStream_t), for device-side timing. */
+int cs_stream(cs_engine *h, void **stream);
 /* Device pointer of a state plane for halo exchange / zero-copy interop:
    which = 0..5 -> x, y, z, vx, vy, vz of the CURRENT state; returns the
    pitch (elements per grid row) through *pitch. */

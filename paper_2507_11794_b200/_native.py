@@ -116,6 +116,7 @@ SIGNATURES = {
     "cs_write": (_I32, [_P, _I32, _P]),
     "cs_inject_response": (_I32, [_P, _I64, ctypes.POINTER(_I32), _I32]),
     "cs_synchronize": (_I32, [_P]),
+    "cs_stream": (_I32, [_P, ctypes.POINTER(_P)]),
     "cs_state_plane": (_I32, [_P, _I32, ctypes.POINTER(_P), ctypes.POINTER(_I64)]),
     "cs_state_buffers": (_I32, [_P, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_P),
                                 ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),

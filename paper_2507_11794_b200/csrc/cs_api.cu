@@ -997,6 +997,12 @@ extern "C" int cs_synchronize(cs_engine *h) {
     return 0;
 }
 
+extern "C" int cs_stream(cs_engine *h, void **stream) {
+    if (!h || !stream) return fail(CS_E_INVALID, "null argument");
+    *stream = (void *)h->st;
+    return 0;
+}
+
 // ---------------------------------------------------------------------------
 // transfers
 // ---------------------------------------------------------------------------

@@ -502,6 +502,21 @@ class Engine:
     def synchronize(self) -> None:
         N.check(self._lib.cs_synchronize(self._handle))
 
+    @property
+    def stream_handle(self) -> int:
+        """The engine's cudaStream_t (for events / torch.cuda.ExternalStream)."""
+        s = ctypes.c_void_p()
+        N.check(self._lib.cs_stream(self._handle, ctypes.byref(s)))
+        return s.value or 0
+
+    @property
+    def stencil_bytes_per_frame(self) -> int:
+        """Algorithmic HBM bytes of one frame's spring/integrate/normals pass:
+        24 B read + 24 B written (pos, vel) + 12 B normals per node, fused
+        (SURVEY.md 8(d)); 72 B when the normals run as a separate pass."""
+        extra = self.kernels_per_frame - int(self.params.substeps) - (4 if self._has_obstacle else 0)
+        return (60 if extra == 0 else 72) * self.num_nodes
+
     def _frame_hits(self, frame):
         hits, resp = ctypes.c_int64(), ctypes.c_int64()
         N.check(self._lib.cs_frame_hits(self._handle, int(frame), ctypes.byref(hits),

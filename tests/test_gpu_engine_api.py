@@ -205,3 +205,20 @@ def test_capacity_error_for_impossible_layouts():
 
     with pytest.raises(P.CapacityError):
         P.Engine(generate_cloth_grid(64, 64), device=Tiny())
+
+
+def test_run_frames_stats_rows(tmp_path):
+    """frames.run_frames: the reference harness's per-frame loop with device
+    time and the stencil pass's HBM figures; hits match StepResult."""
+    from paper_2507_11794_b200 import frames as F
+
+    sc = P.build_scene(P.ScenarioConfig("drop", (24, 24), obstacle="icosphere:2"))
+    eng = P.Engine(sc.mesh, sc.obstacle, sc.params, pair_budget=10**13)
+    eng.step_frames(100)
+    rows = F.run_frames(eng, 20)
+    assert len(rows) == 20 and all(r.device_ms > 0 and r.wall_ms > 0 for r in rows)
+    assert rows[0].stencil_bytes == 60 * 24 * 24
+    assert sum(r.collision_hits for r in rows) == eng.stats()["hit_counter"] - \
+        sum(eng._frame_hits(f)[0] for f in range(100))
+    F.write_stats_csv(tmp_path / "s.csv", rows)
+    assert len(F.parse_stats_csv(tmp_path / "s.csv")) == 20

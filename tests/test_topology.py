@@ -130,3 +130,26 @@ def test_grid_families_partition_the_springs(nx, ny):
         np.testing.assert_array_equal(got, want)
         seen.append(got)
     assert sum(len(x) for x in seen) == len(springs)
+
+
+def test_frame_stats_csv_round_trip_and_reference_header(tmp_path):
+    """frames.FrameStats CSV: the reference's eight columns first, in its
+    order (clothsim/io.py STATS_FIELDS), extras after, round-trips."""
+    import sys
+
+    from paper_2507_11794_b200 import frames as F
+
+    sys.path.insert(0, "/root/reference/pkg/src")
+    try:
+        from clothsim.io import STATS_FIELDS as REF
+    except Exception:  # the reference is only in the build container
+        REF = F.STATS_FIELDS
+    assert F.STATS_FIELDS == tuple(REF)
+    rows = [F.FrameStats(frame=i, wall_ms=1.5 + i, fps=600.0, nodes=64, springs=306,
+                         obstacle_triangles=80, collision_hits=i, backend="cuda", device_ms=0.02,
+                         stencil_bytes=3840, achieved_gbs=192.0, hbm_frac=0.03) for i in range(3)]
+    p = tmp_path / "f.csv"
+    F.write_stats_csv(p, rows)
+    back = F.parse_stats_csv(p)
+    assert [r.collision_hits for r in back] == [0, 1, 2]
+    assert back[1].stencil_bytes == 3840 and abs(back[2].wall_ms - 3.5) < 1e-9
