@@ -794,7 +794,7 @@ k_detect_warp(const CollideArgs A, const GridDesc g, const uint32_t *__restrict_
 // other two mappings, so the hit set and the integer accumulators are
 // identical.
 // ---------------------------------------------------------------------------
-constexpr int BATCH_WARPS = 8;
+constexpr int BATCH_WARPS = 4;
 struct QuerySlot {
     float v[3][3];
     float lo[3], hi[3];   // query box (PASS 0: padded segment box; PASS 1: tri box +- 2 pad)
