@@ -281,6 +281,9 @@ static Detect64Args detect64_args(const cs_engine *h) {
     D.eps = h->eps64;
     D.margin = h->margin64;
     D.pad = 1e-5f;
+    D.clog = h->clog;
+    D.clog_n = h->clog_n;
+    D.clog_cap = (uint32_t)h->clog_cap;
     return D;
 }
 
@@ -292,6 +295,7 @@ static void pass_detect(cs_engine *h) {
         // the float64 path synchronises: its contact count sizes the sort,
         // and an overflowing pass is re-run with larger buffers
         for (;;) {
+            if (h->clog) cudaMemsetAsync(h->clog_n, 0, sizeof(uint32_t), h->st);
             launch_detect64(h->c64, detect64_args(h), h->bp, h->edges_g, h->ne, h->tris_g, h->nc,
                             h->stats, h->st);
             cudaMemcpyAsync(&h->c64_n, h->c64.count, sizeof(uint32_t), cudaMemcpyDeviceToHost, h->st);

@@ -73,8 +73,15 @@ __device__ __forceinline__ void offset64(const double *p, const double *hit, con
     out[2] = dmul(n[2], scale);
 }
 
-__device__ __forceinline__ void emit(const Detect64Args &D, uint32_t node, uint64_t key,
-                                     const double *off) {
+__device__ __forceinline__ void emit(const Detect64Args &D, uint32_t node, uint32_t tri,
+                                     uint64_t key, const double *off) {
+    if (D.clog) {
+        const uint32_t slot = atomicAdd(D.clog_n, 1u);
+        if (slot < D.clog_cap) {
+            D.clog[2 * slot] = node;
+            D.clog[2 * slot + 1] = tri;
+        }
+    }
     const uint32_t k = atomicAdd(D.count, 1u);
     if (k >= D.cap) return;  // overflow: the host grows the buffers and re-runs
     D.node[k] = node;
@@ -160,9 +167,9 @@ k_detect64(const Detect64Args D, const GridDesc g, const uint32_t *__restrict__ 
                         const uint64_t base = ((uint64_t)q * (uint64_t)D.nt + t) * 2u;
                         double off[3];
                         offset64(v[0], hit, fn, sign, D.margin, off);
-                        emit(D, (uint32_t)nid[0], base, off);
+                        emit(D, (uint32_t)nid[0], t, base, off);
                         offset64(v[1], hit, fn, sign, D.margin, off);
-                        emit(D, (uint32_t)nid[1], base + 1, off);
+                        emit(D, (uint32_t)nid[1], t, base + 1, off);
                     } else {
                         for (int slot = 0; slot < 3; ++slot) {
                             const double *ea = cr + 3 * slot;
@@ -182,7 +189,7 @@ k_detect64(const Detect64Args D, const GridDesc g, const uint32_t *__restrict__ 
                             double off[3];
                             for (int k = 0; k < 3; ++k) {
                                 offset64(v[k], hit, fn, sign, D.margin, off);
-                                emit(D, (uint32_t)nid[k], base + k, off);
+                                emit(D, (uint32_t)nid[k], t, base + k, off);
                             }
                         }
                     }

@@ -17,6 +17,9 @@ struct Detect64Args {
     double *off;
     uint32_t *count;
     uint32_t cap;
+    // optional (node, obstacle triangle) contact log (cs_contact_log)
+    uint32_t *clog, *clog_n;
+    uint32_t clog_cap;
 };
 
 // Contact buffers: node, serial-order key (hi/lo words), offset, plus sort

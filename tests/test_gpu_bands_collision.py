@@ -48,6 +48,28 @@ def test_banded_run_is_bit_identical_to_one_engine(world, precision):
     np.testing.assert_array_equal(got, whole.read_positions())
 
 
+def _assert_diff_on_boundary(diff, mesh, obstacle, pos, tol=1e-5):
+    """Every (node, triangle) pair in `diff` has a segment-triangle test whose
+    predicate quantities lie within `tol` of a decision boundary
+    (oracle.boundary_distance, tests/oracles.py:81-116)."""
+    from oracle import oracle as O
+
+    tris = np.asarray(mesh.triangles)
+    ov, ot = obstacle.vertices, obstacle.triangles
+    p64 = pos.astype(np.float64)
+    for node, t in diff:
+        cand = []
+        for c in np.nonzero((tris == node).any(axis=1))[0]:
+            a, b, d = tris[c]
+            for u, w in ((a, b), (b, d), (d, a)):  # cloth edges through the node
+                if node in (u, w):
+                    cand.append(O.boundary_distance(p64[u], p64[w], *ov[ot[t]]))
+            for s in range(3):  # obstacle edges of t vs this cloth triangle
+                cand.append(O.boundary_distance(ov[ot[t][s]], ov[ot[t][(s + 1) % 3]],
+                                                p64[a], p64[b], p64[d]))
+        assert min(cand) < tol, (node, t, min(cand))
+
+
 @pytest.mark.parametrize("spec", [("icosphere:2", (24, 24), 120), ("uvsphere:40x40", (64, 64), 90)])
 def test_contact_set_matches_f64_solver_except_boundary_pairs(spec):
     """North-star contact gate: the (node, triangle) contact set of a GPU
@@ -75,21 +97,36 @@ def test_contact_set_matches_f64_solver_except_boundary_pairs(spec):
     ref = Counter(map(tuple, ref_arr.tolist()))
     assert hits > 0 and sum(ref.values()) > 0
     diff = (gpu - ref) + (ref - gpu)
-    tris = np.asarray(sc.mesh.triangles)
-    ov, ot = sc.obstacle.vertices, sc.obstacle.triangles
-    p64 = pos.astype(np.float64)
-    for node, t in diff:
-        cand = []
-        for c in np.nonzero((tris == node).any(axis=1))[0]:
-            a, b, d = tris[c]
-            for u, w in ((a, b), (b, d), (d, a)):  # cloth edges through the node
-                if node in (u, w):
-                    cand.append(O.boundary_distance(p64[u], p64[w], *ov[ot[t]]))
-            for s in range(3):  # obstacle edges of t vs this cloth triangle
-                cand.append(O.boundary_distance(ov[ot[t][s]], ov[ot[t][(s + 1) % 3]],
-                                                p64[a], p64[b], p64[d]))
-        assert min(cand) < 1e-5, (node, t, min(cand))
+    _assert_diff_on_boundary(diff, sc.mesh, sc.obstacle, pos)
     assert sum(diff.values()) <= max(4, 0.01 * sum(ref.values()))
+
+
+def test_contact_set_at_c3_scale_against_the_solver_exact_fp64_engine():
+    """The contact gate at full C3 size (316^2 cloth draped on the 99,904-
+    triangle sphere): the fast engine's contact set against the float64
+    engine's, which is bit-identical to the reference solver (golden
+    trajectories with obstacles), at the same positions."""
+    from collections import Counter
+
+    from paper_2507_11794_b200 import _native as N
+
+    sc = P.baseline_scene("C3")
+    fast = P.Engine(sc.mesh, sc.obstacle, sc.params, pair_budget=10**13)
+    fast.step_frames(300)
+    fast.enable_contact_log(1 << 22)
+    N.check(fast._lib.cs_run_pass(fast._handle, N.PASS_FORCE_INTEGRATE))
+    pos = fast.read_positions()
+    N.check(fast._lib.cs_run_pass(fast._handle, N.PASS_DETECT))
+    got = Counter(map(tuple, fast.read_contacts().tolist()))
+    ref = P.Engine(sc.mesh, sc.obstacle, sc.params, pair_budget=10**13, precision="fp64")
+    ref.write_state64(pos=pos.astype(np.float64))
+    ref.enable_contact_log(1 << 22)
+    N.check(ref._lib.cs_run_pass(ref._handle, N.PASS_DETECT))
+    want = Counter(map(tuple, ref.read_contacts().tolist()))
+    assert sum(want.values()) > 10_000
+    diff = (got - want) + (want - got)
+    _assert_diff_on_boundary(diff, sc.mesh, sc.obstacle, pos)
+    assert sum(diff.values()) <= max(4, 0.001 * sum(want.values()))
 
 
 def test_c3_drapes_finite_with_contacts_in_both_modes():
