@@ -861,22 +861,29 @@ __device__ __forceinline__ uint32_t narrow_item(const CollideArgs &A, const Quer
 
 constexpr int QCAP = 128;  // per-warp item queue: < 32 left + 32 lanes x 3 slots
 
-template <int PASS>
-__global__ void __launch_bounds__(32 * BATCH_WARPS)
-k_detect_batch(const CollideArgs A, const GridDesc g, const uint2 *__restrict__ cbe,
-               const float4 *__restrict__ rbox, const float *__restrict__ corners,
-               const float *__restrict__ normals, const int32_t *__restrict__ items, int64_t nq,
-               int qb) {
-    __shared__ QuerySlot slots[BATCH_WARPS][32];
+struct BatchShared {
+    QuerySlot slots[BATCH_WARPS][32];
     // items that survived the box / dedup (/ edge box) filters wait here until
     // a full warp's worth can run the predicate with every lane active
-    __shared__ uint32_t qtri[BATCH_WARPS][QCAP];
-    __shared__ uint8_t qmeta[BATCH_WARPS][QCAP];  // query slot << 2 | edge slot
+    uint32_t qtri[BATCH_WARPS][QCAP];
+    uint8_t qmeta[BATCH_WARPS][QCAP];  // query slot << 2 | edge slot
+};
+
+template <int PASS>
+__device__ __forceinline__ void detect_batch(BatchShared &S, int64_t blk, const CollideArgs &A,
+                                             const GridDesc &g, const uint2 *__restrict__ cbe,
+                                             const float4 *__restrict__ rbox,
+                                             const float *__restrict__ corners,
+                                             const float *__restrict__ normals,
+                                             const int32_t *__restrict__ items, int64_t nq, int qb) {
+    auto &slots = S.slots;
+    auto &qtri = S.qtri;
+    auto &qmeta = S.qmeta;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
     // qb queries per warp (lanes >= qb hold none): 32 when queries are
     // plentiful, fewer so that small clouds still spread over every SM
-    const int64_t q = (blockIdx.x * (int64_t)BATCH_WARPS + w) * qb + lane;
+    const int64_t q = (blk * BATCH_WARPS + w) * qb + lane;
     QuerySlot &my = slots[w][lane];
     const int nv = PASS == 0 ? 2 : 3;
     uint32_t ncell = 0;
@@ -1016,6 +1023,22 @@ k_detect_batch(const CollideArgs A, const GridDesc g, const uint2 *__restrict__ 
     count_hits(A.frame_hits, hits);
 }
 
+// Both passes in ONE launch: blocks [0, blocks_a) take cloth edges (pass A),
+// the rest cloth triangles (pass B) -- no dependency between them, one
+// launch latency instead of two.
+__global__ void __launch_bounds__(32 * BATCH_WARPS)
+k_detect_batch(const CollideArgs A, const GridDesc g, const uint2 *__restrict__ cbe,
+               const float4 *__restrict__ rbox, const float *__restrict__ corners,
+               const float *__restrict__ normals, const int32_t *__restrict__ edges, int64_t ne,
+               int qb_a, int64_t blocks_a, const int32_t *__restrict__ tris, int64_t nc, int qb_b) {
+    __shared__ BatchShared S;
+    if ((int64_t)blockIdx.x < blocks_a)
+        detect_batch<0>(S, blockIdx.x, A, g, cbe, rbox, corners, normals, edges, ne, qb_a);
+    else
+        detect_batch<1>(S, blockIdx.x - blocks_a, A, g, cbe, rbox, corners, normals, tris, nc,
+                        qb_b);
+}
+
 __global__ void k_tri_boxes(int64_t nt, const float *__restrict__ corners, float *__restrict__ box) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= nt) return;
@@ -1043,18 +1066,13 @@ void launch_detect(const CollideArgs &A, const BroadPhase &bp, const float *corn
             while (qb > 1 && nq / qb < (int64_t)148 * 48) qb >>= 1;
             return qb;
         };
-        if (ne > 0) {
-            const int qb = qb_for(ne);
-            const int64_t warps = (ne + qb - 1) / qb;
-            k_detect_batch<0><<<nblk(warps, BATCH_WARPS), 32 * BATCH_WARPS, 0, st>>>(
-                A, bp.grid, bp.cell_be, bp.ref_box, corners, normals, edges, ne, qb);
-        }
-        if (nc > 0) {
-            const int qb = qb_for(nc);
-            const int64_t warps = (nc + qb - 1) / qb;
-            k_detect_batch<1><<<nblk(warps, BATCH_WARPS), 32 * BATCH_WARPS, 0, st>>>(
-                A, bp.grid, bp.cell_be, bp.ref_box, corners, normals, tris, nc, qb);
-        }
+        const int qa = qb_for(ne), qc = qb_for(nc);
+        const int64_t ba = ne > 0 ? nblk((ne + qa - 1) / qa, BATCH_WARPS) : 0;
+        const int64_t bc = nc > 0 ? nblk((nc + qc - 1) / qc, BATCH_WARPS) : 0;
+        if (ba + bc > 0)
+            k_detect_batch<<<(unsigned)(ba + bc), 32 * BATCH_WARPS, 0, st>>>(
+                A, bp.grid, bp.cell_be, bp.ref_box, corners, normals, edges, ne, qa, ba, tris, nc,
+                qc);
         return;
     }
     if (bp.warp_per_query) {
