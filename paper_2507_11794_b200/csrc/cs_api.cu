@@ -104,7 +104,7 @@ struct cs_engine {
     Contacts64 c64;
     uint32_t c64_n = 0;
     int32_t *acc = nullptr, *count = nullptr;
-    uint32_t *touched = nullptr, *touched_n = nullptr;
+    uint32_t *touched = nullptr, *touched_n = nullptr, *respond_done = nullptr;
     // [frame_hits, frame_responded, hit_counter, frame_counter, ring (2 x kRing)]
     unsigned long long *stats = nullptr;
     static constexpr int kRing = 4096;
@@ -144,6 +144,7 @@ struct cs_engine {
         A.count = count;
         A.touched = touched;
         A.touched_n = touched_n;
+        A.blocks_done = respond_done;
         A.frame_hits = stats;
         A.frame_responded = stats + 1;
         A.hit_counter = stats + 2;
@@ -164,7 +165,9 @@ struct cs_engine {
     }
     int kernels_per_frame() const {
         int k = substeps;  // one fused force+integrate launch per substep
-        if (has_obstacle) k += 2 /*detect*/ + 2 /*respond + frame_end*/;
+        // detect: both passes in one launch (batched narrow phase) or two;
+        // respond closes the frame in its last block
+        if (has_obstacle) k += (bp.warp_per_query == 2 ? 1 : 2) + 1;
         if (!fuse_normals()) k += grid ? 1 : 2;  // normals (else fused into the strip kernel)
         return k;
     }
@@ -728,6 +731,8 @@ static int build(cs_engine *h, const cs_desc *d) {
     CK(dalloc(&h->count, P));
     CK(dalloc(&h->touched, P));
     CK(dalloc(&h->touched_n, 1));
+    CK(dalloc(&h->respond_done, 1));
+    CK(cudaMemsetAsync(h->respond_done, 0, 4, h->st));
     CK(cudaMemsetAsync(h->acc, 0, 3 * P * 4, h->st));
     CK(cudaMemsetAsync(h->count, 0, P * 4, h->st));
     CK(cudaMemsetAsync(h->touched_n, 0, 4, h->st));
@@ -768,7 +773,8 @@ extern "C" int cs_destroy(cs_engine *h) {
                     h->pinned8, h->ext, h->forces_raw, h->csr_off, h->csr_nbr, h->csr_kind,
                     h->csr_rest, h->csr_rest64, h->inc_off, h->inc_tri, h->face, h->tris_g,
                     h->edges_g, h->corners, h->onormals, h->acc, h->count, h->touched,
-                    h->touched_n, h->stats, h->stage, h->hflags, h->corners64, h->onormals64};
+                    h->touched_n, h->stats, h->stage, h->hflags, h->corners64, h->onormals64,
+                    h->respond_done};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (h->has_obstacle) free_broadphase(h->bp);

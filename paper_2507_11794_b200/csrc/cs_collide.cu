@@ -595,9 +595,11 @@ k_detect_obstacle_edges(const CollideArgs A, const GridDesc g, const uint32_t *_
 // Respond (kernels.py:293-311) over the touched list only: every node with a
 // nonzero count is on the list exactly once.  Flip-and-halve the velocity,
 // add the decoded (optionally averaged) offset, clear the accumulators.
+__device__ __forceinline__ void respond_end(const CollideArgs &A, int end_of_frame);
+
 __global__ void __launch_bounds__(256)
 k_respond(const CollideArgs A, float *__restrict__ pos, const uint32_t *__restrict__ pinbits,
-          const float *__restrict__ inv_mass, int average) {
+          const float *__restrict__ inv_mass, int average, int end_of_frame) {
     const uint32_t n = *A.touched_n;
     uint32_t moved = 0;
     for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
@@ -620,21 +622,38 @@ k_respond(const CollideArgs A, float *__restrict__ pos, const uint32_t *__restri
         A.count[g] = 0;
     }
     count_hits(A.frame_responded, moved);
+    // the last block to finish closes the frame (no separate launch)
+    __shared__ int last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(A.blocks_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        *A.blocks_done = 0;
+        respond_end(A, end_of_frame);
+    }
 }
 
 // After the respond pass: clear the touched list; at the end of a frame also
 // fold the frame's hits into the cumulative hitCounter and record
 // (hits, responded) in the per-frame ring that StepResult reads lazily.
-__global__ void k_respond_end(const CollideArgs A, int end_of_frame) {
+__device__ __forceinline__ void respond_end(const CollideArgs &A, int end_of_frame) {
     *A.touched_n = 0;
     if (end_of_frame) {
         const unsigned long long f = *A.frame_counter;
-        *A.hit_counter += *A.frame_hits;
-        A.ring[2 * (f % A.ring_size)] = *A.frame_hits;
-        A.ring[2 * (f % A.ring_size) + 1] = *A.frame_responded;
+        const unsigned long long hits = atomicAdd(A.frame_hits, 0ull);
+        const unsigned long long resp = atomicAdd(A.frame_responded, 0ull);
+        *A.hit_counter += hits;
+        A.ring[2 * (f % A.ring_size)] = hits;
+        A.ring[2 * (f % A.ring_size) + 1] = resp;
         *A.frame_counter = f + 1;
     }
 }
+
+__global__ void k_respond_end(const CollideArgs A, int end_of_frame) { respond_end(A, end_of_frame); }
 
 // Rebuild the touched list from the count buffer (after host writes).
 __global__ void k_rebuild_touched(const CollideArgs A, int64_t n_rows, int64_t nx, int64_t pitch) {
@@ -1102,8 +1121,8 @@ void launch_respond(const CollideArgs &A, float *state, const uint32_t *pinbits,
     const int64_t cap = (int64_t)num_sms * 8;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    k_respond<<<(unsigned)blocks, 256, 0, st>>>(A, state, pinbits, inv_mass, average);
-    k_respond_end<<<1, 1, 0, st>>>(A, end_of_frame ? 1 : 0);
+    k_respond<<<(unsigned)blocks, 256, 0, st>>>(A, state, pinbits, inv_mass, average,
+                                                 end_of_frame ? 1 : 0);
 }
 
 void launch_respond_end(const CollideArgs &A, bool end_of_frame, cudaStream_t st) {

@@ -67,6 +67,7 @@ struct CollideArgs {
     int32_t *count;         // 1 plane (responseCount)
     uint32_t *touched;      // nodes whose count went 0 -> 1 this frame
     uint32_t *touched_n;
+    uint32_t *blocks_done;            // k_respond's last-block counter (self-resetting)
     unsigned long long *frame_hits;
     unsigned long long *frame_responded;
     unsigned long long *hit_counter;  // cumulative hitCounter

@@ -377,6 +377,7 @@ class Engine:
         self._handle = h
         self.kparams = d  # the baked parameter block (engine.py:274-285 KernelParams)
         self.stencil = stencil is not None and not force_csr and precision != "fp64"
+        self._fused_normals = self.stencil and kernel != "tile" and normals != "split"
         self.frame_count = 0
         self.buffers = PipelineBuffers(self)
         self._has_obstacle = has_obs
@@ -514,8 +515,7 @@ class Engine:
         """Algorithmic HBM bytes of one frame's spring/integrate/normals pass:
         24 B read + 24 B written (pos, vel) + 12 B normals per node, fused
         (SURVEY.md 8(d)); 72 B when the normals run as a separate pass."""
-        extra = self.kernels_per_frame - int(self.params.substeps) - (4 if self._has_obstacle else 0)
-        return (60 if extra == 0 else 72) * self.num_nodes
+        return (60 if self._fused_normals else 72) * self.num_nodes
 
     def _frame_hits(self, frame):
         hits, resp = ctypes.c_int64(), ctypes.c_int64()
