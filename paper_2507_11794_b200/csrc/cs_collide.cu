@@ -258,14 +258,20 @@ __global__ void k_pack_cells(int64_t n, const uint32_t *__restrict__ beg,
     if (i < n) be[i] = make_uint2(beg[i], end[i]);
 }
 
-__global__ void k_ref_boxes(int64_t n, const uint32_t *__restrict__ tris,
+// per sorted reference: its triangle's box, the triangle id (lo.w) and the
+// grid cell of the box's minimum corner packed 10:10:10 (hi.w) -- the dedup
+// test then needs no cell_of per candidate, because cell_of is monotone:
+// cell_of(max(q_lo, t_lo)) == max(cell_of(q_lo), cell_of(t_lo)).
+__global__ void k_ref_boxes(const GridDesc g, int64_t n, const uint32_t *__restrict__ tris,
                             const float *__restrict__ tbox, float4 *__restrict__ out) {
     const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r >= n) return;
     const uint32_t t = tris[r];
     const float *b = tbox + 6 * (int64_t)t;
+    const uint32_t cell = (uint32_t)g.cell_of(b[0], 0) | ((uint32_t)g.cell_of(b[1], 1) << 10) |
+                          ((uint32_t)g.cell_of(b[2], 2) << 20);
     out[2 * r] = make_float4(b[0], b[1], b[2], __uint_as_float(t));
-    out[2 * r + 1] = make_float4(b[3], b[4], b[5], 0.f);
+    out[2 * r + 1] = make_float4(b[3], b[4], b[5], __uint_as_float(cell));
 }
 
 int build_broadphase(BroadPhase &bp, const float *d_corners, int64_t nt, const float *h_corners,
@@ -349,7 +355,8 @@ int build_broadphase(BroadPhase &bp, const float *d_corners, int64_t nt, const f
     k_pack_cells<<<nblk(bp.num_cells, 256), 256, 0, st>>>(bp.num_cells, bp.cell_begin, bp.cell_end,
                                                           bp.cell_be);
     if (total > 0)
-        k_ref_boxes<<<nblk(total, 256), 256, 0, st>>>(total, bp.cell_tris, bp.tri_box, bp.ref_box);
+        k_ref_boxes<<<nblk(total, 256), 256, 0, st>>>(g, total, bp.cell_tris, bp.tri_box, bp.ref_box);
+    bp.packed_cells = dims[0] <= 1024 && dims[1] <= 1024 && dims[2] <= 1024;
     cudaFree(tv);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
@@ -894,7 +901,8 @@ __device__ __forceinline__ void detect_batch(BatchShared &S, int64_t blk, const 
                                              const float4 *__restrict__ rbox,
                                              const float *__restrict__ corners,
                                              const float *__restrict__ normals,
-                                             const int32_t *__restrict__ items, int64_t nq, int qb) {
+                                             const int32_t *__restrict__ items, int64_t nq, int qb,
+                                             bool packed) {
     auto &slots = S.slots;
     auto &qtri = S.qtri;
     auto &qmeta = S.qmeta;
@@ -1008,10 +1016,18 @@ __device__ __forceinline__ void detect_batch(BatchShared &S, int64_t blk, const 
                 const float tlo[3] = {b0.x, b0.y, b0.z}, thi[3] = {b1.x, b1.y, b1.z};
                 // box test, then dedup: the minimum corner of the intersection
                 // lies in this cell
-                ok = box_overlap(Q.lo, Q.hi, tlo, thi) &&
-                     g.cell_of(fmaxf(Q.lo[0], tlo[0]), 0) == ox &&
-                     g.cell_of(fmaxf(Q.lo[1], tlo[1]), 1) == oy &&
-                     g.cell_of(fmaxf(Q.lo[2], tlo[2]), 2) == oz;
+                if (packed) {
+                    const uint32_t tc = __float_as_uint(b1.w);
+                    ok = box_overlap(Q.lo, Q.hi, tlo, thi) &&
+                         max(Q.a[0], (int)(tc & 1023u)) == ox &&
+                         max(Q.a[1], (int)((tc >> 10) & 1023u)) == oy &&
+                         max(Q.a[2], (int)(tc >> 20)) == oz;
+                } else {
+                    ok = box_overlap(Q.lo, Q.hi, tlo, thi) &&
+                         g.cell_of(fmaxf(Q.lo[0], tlo[0]), 0) == ox &&
+                         g.cell_of(fmaxf(Q.lo[1], tlo[1]), 1) == oy &&
+                         g.cell_of(fmaxf(Q.lo[2], tlo[2]), 2) == oz;
+                }
             }
             if (PASS == 0) {
                 push(ok, tri, qq, 0);
@@ -1049,13 +1065,15 @@ __global__ void __launch_bounds__(32 * BATCH_WARPS)
 k_detect_batch(const CollideArgs A, const GridDesc g, const uint2 *__restrict__ cbe,
                const float4 *__restrict__ rbox, const float *__restrict__ corners,
                const float *__restrict__ normals, const int32_t *__restrict__ edges, int64_t ne,
-               int qb_a, int64_t blocks_a, const int32_t *__restrict__ tris, int64_t nc, int qb_b) {
+               int qb_a, int64_t blocks_a, const int32_t *__restrict__ tris, int64_t nc, int qb_b,
+               int packed) {
     __shared__ BatchShared S;
     if ((int64_t)blockIdx.x < blocks_a)
-        detect_batch<0>(S, blockIdx.x, A, g, cbe, rbox, corners, normals, edges, ne, qb_a);
+        detect_batch<0>(S, blockIdx.x, A, g, cbe, rbox, corners, normals, edges, ne, qb_a,
+                        packed != 0);
     else
         detect_batch<1>(S, blockIdx.x - blocks_a, A, g, cbe, rbox, corners, normals, tris, nc,
-                        qb_b);
+                        qb_b, packed != 0);
 }
 
 __global__ void k_tri_boxes(int64_t nt, const float *__restrict__ corners, float *__restrict__ box) {
@@ -1091,7 +1109,7 @@ void launch_detect(const CollideArgs &A, const BroadPhase &bp, const float *corn
         if (ba + bc > 0)
             k_detect_batch<<<(unsigned)(ba + bc), 32 * BATCH_WARPS, 0, st>>>(
                 A, bp.grid, bp.cell_be, bp.ref_box, corners, normals, edges, ne, qa, ba, tris, nc,
-                qc);
+                qc, bp.packed_cells ? 1 : 0);
         return;
     }
     if (bp.warp_per_query) {

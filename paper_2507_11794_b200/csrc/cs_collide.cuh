@@ -56,6 +56,7 @@ struct BroadPhase {
     // one 32-byte load per candidate instead of ctri -> tri_box
     uint2 *cell_be = nullptr;
     float4 *ref_box = nullptr;
+    bool packed_cells = false;       // every grid axis <= 1024 cells (10-bit packing)
     int warp_per_query = 2;          // narrow phase: 32-query batches per warp (2),
                                      // warp per query (1) or thread per query (0)
 };
