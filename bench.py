@@ -285,6 +285,7 @@ def main():
                         "note": "back-to-back graph replays, state stays in the 126 MB L2"},
         "roofline": {"bound": "hbm", "kernel": KERNEL_NAME,
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "frac_of_spec_8tbs": achieved / SPEC_HBM_GBS,
                      "traffic": traffic, "bytes_per_launch": alg_bytes,
                      "bytes_per_node": FRAME_BYTES_PER_NODE, "launch_ms": ms,
                      "peak_source": peak_src,
@@ -302,6 +303,7 @@ def main():
     print(json.dumps(line))
 
 
+SPEC_HBM_GBS = 8000.0  # B200 datasheet HBM3e bandwidth (SURVEY.md 8(d) asks for both)
 FRAME_BYTES_PER_NODE = 60  # 24 B read + 24 B written (pos, vel) + 12 B normals written
 KERNEL_NAME = "k_pair3<NORMALS=1> (fused spring force + integrate + previous frame's normals)"
 
@@ -354,7 +356,8 @@ def c5_roofline(P, torch, stream, args):
             "steps_per_s": 1000.0 / frame_ms, "frame_ms": frame_ms, "kernels_per_frame": kpf,
             "kernel": KERNEL_NAME, "launch_ms": frame_ms / kpf if kpf == 1 else None,
             "bound": "hbm", "achieved": frame_gbs, "peak": peak, "unit": "GB/s",
-            "frac": frame_gbs / peak, "bytes_per_launch": frame_bytes,
+            "frac": frame_gbs / peak, "frac_of_spec_8tbs": frame_gbs / SPEC_HBM_GBS,
+            "bytes_per_launch": frame_bytes,
             "bytes_per_node": frame_bytes // n, "traffic": _traffic("C5_frame"),
             "force_integrate": {"kernel": "k_pair3<NORMALS=0> (spring force + integrate only, "
                                           "cs_run_pass FORCE_INTEGRATE)",
