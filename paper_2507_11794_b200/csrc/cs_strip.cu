@@ -1,6 +1,8 @@
-// cs_strip.cu -- the production grid kernel: fused spring force + integrate
-// (+ the previous frame's vertex normals), one warp per 28-column x 64-row
-// strip, no shared memory, no block barriers.
+// cs_strip.cu -- the scalar warp-strip grid kernel: fused spring force +
+// integrate (+ the previous frame's vertex normals), one warp per 28-column
+// x 64-row strip, no shared memory, no block barriers.  It serves the
+// reference-exact fixed-point mode and Engine(kernel="strip"); the fast
+// default is its paired-column successor in cs_pair3.cu.
 //
 // Reference semantics: gpu/kernels.py:86-133 (spring_force + integrate) and
 // :314-339 (normal_update) on the grid topology of mesh.py:274-305.
