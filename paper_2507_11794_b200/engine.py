@@ -13,13 +13,15 @@ constructor raises ``AdapterUnavailable``.
 
 Arithmetic modes (keyword-only ``precision=``):
 
-* ``"fast"`` (default) -- fp32 node gather with the 12-spring grid stencil;
-  parity with the reference CPU solver within the north star's tolerances.
+* ``"fast"`` (default) -- fp32 warp-strip stencil (six forward springs per
+  node, exact reaction exchange, paired FFMA2 math); parity with the
+  reference CPU solver within the north star's tolerances, collision in the
+  reference engine's exact f32 arithmetic.
 * ``"fixed"`` -- the reference engine's arithmetic (per-spring f32 force,
   i32 fixed point at ``fixed_point_scale``): bit-identical to the reference's
   ``gpu.engine.Engine`` in every buffer, hit count and contact.
-* ``"fp64"`` -- float64 gather in the reference solver's operation order:
-  bit-identical to ``solver.step`` (no obstacle).
+* ``"fp64"`` -- float64 gather and collision in the reference solver's
+  operation order: bit-identical to ``solver.step``, obstacles included.
 """
 
 from __future__ import annotations
@@ -309,8 +311,8 @@ class Engine:
         if force_csr:
             flags |= N.FLAG_FORCE_CSR
         if kernel not in ("strip", "pair", "tile"):
-            raise ValueError("kernel must be 'strip' (warp strips, default), 'pair' "
-                             "(paired-column f32x2 warp strips) or 'tile' (shared-memory tiles)")
+            raise ValueError("kernel must be 'pair' (paired-column f32x2 warp strips, default), "
+                             "'strip' (scalar warp strips) or 'tile' (shared-memory tiles)")
         if kernel == "tile":
             flags |= N.FLAG_TILE_KERNEL
         if normals not in ("auto", "fused", "split"):
