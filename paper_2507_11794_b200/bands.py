@@ -392,7 +392,10 @@ def run_banded_bench(args, metric, clock_sampler=None, peak=None):
                                          "flag handshake (CUDA IPC over NVLink)"
                                          if exchange == "p2p" else
                                          "torch.distributed NCCL send/recv after each step"),
-                       "l2": "inputs (16.8M nodes, 805 MB/step) larger than L2"},
+                       "l2": "inputs (16.8M nodes, 805 MB/step) larger than L2",
+                       "scaling_baseline": ("the same C5 workload on 1 GPU is roofline_c5."
+                                            "steps_per_s in the N=1 line, whose headline "
+                                            "value is C2 (the metric's named config)")},
             "node_updates_per_s": 1000.0 / ms * n * n,
             "roofline": {"bound": "hbm", "kernel": "k_pair3<NORMALS=1> on rank 0's band",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
