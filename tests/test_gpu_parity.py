@@ -253,3 +253,24 @@ def test_debug_step_snapshots_and_hits_match_oracle():
         saw |= r.hits > 0
     assert saw
     np.testing.assert_array_equal(eng.read_positions(), eo.pos)
+
+
+def test_c5_fast_mode_against_the_solver_exact_fp64_engine():
+    """The tolerance gates at full C5 size (16.8M nodes), against the float64
+    engine (bit-identical to solver.step on every golden trajectory): one
+    step from the same state within 1e-5 of extent, 100 steps within 1e-3."""
+    sc = P.baseline_scene("C5")
+    ext = _extent(sc.mesh)
+    fast = P.Engine(sc.mesh, params=sc.params)
+    ref = P.Engine(sc.mesh, params=sc.params, precision="fp64")
+    fast.step()
+    ref.step()
+    d1 = np.abs(fast.read_positions().astype(np.float64) - ref.read_positions64()).max()
+    v1 = np.abs(fast.read_velocities().astype(np.float64) - ref.read_velocities64()).max()
+    assert d1 <= 1e-5 * ext and v1 <= 1e-5 * ext, (d1, v1)
+    fast.step_frames(99)
+    ref.step_frames(99)
+    d100 = np.abs(fast.read_positions().astype(np.float64) - ref.read_positions64()).max()
+    assert d100 <= 1e-3 * ext, d100
+    fast.close()
+    ref.close()
