@@ -565,7 +565,11 @@ static int build(cs_engine *h, const cs_desc *d) {
     sp.k_shear = (float)d->stiffness[1];
     sp.k_bend = (float)d->stiffness[2];
     sp.damping = (float)d->damping;
-    for (int q = 0; q < 6; ++q) sp.rest[q] = d->grid_rest[q];
+    for (int q = 0; q < 6; ++q) {
+        sp.rest[q] = d->grid_rest[q];
+        const double kq = q < 2 ? sp.k_struct : (q < 4 ? sp.k_shear : sp.k_bend);
+        sp.nkr2[q] = (float)(-kq * (double)sp.rest[q] * (double)sp.rest[q]);
+    }
     sp.inv_mass = im_free;
     sp.scale_f = (float)d->fixed_point_scale;
     sp.scale_d = (double)d->fixed_point_scale;
