@@ -249,6 +249,25 @@ int cs_broadphase_stats(cs_engine *h, int64_t out[4]);
 int cs_device_count(void);
 /* Free / total device memory, for the capacity check (gpu/layout.py:192-202). */
 int cs_mem_info(int64_t *free_bytes, int64_t *total_bytes);
+/* Orthographic depth-shaded snapshot (replaces clothsim/io.py:225-287
+   snapshot_png and :187-222 _rasterize), rendered on the device.  All
+   pointers are DEVICE pointers.  verts: f64 (n, 3) -- the cloth vertices,
+   then the obstacle's; tris: int32 (num_tris, 3) into verts -- the cloth's
+   triangles first (material 1, num_cloth_tris of them), then the obstacle's
+   (material 2).  cs_snapshot_bounds returns min xyz, max xyz of verts (host
+   out[6]); the caller pads them and forms view = {lo_u, lo_v, scale} exactly
+   as io.py:249-258 does.  axes = {u, v, depth} coordinate indices (io.py
+   _VIEW_AXES).  rgb: u8 (height, width, 3); scratch: (2*width*height + 2)
+   u64.  Bit-identical pixels to the reference (float64, numpy's operation
+   order, strict-greater z test with earlier-triangle ties). */
+int cs_snapshot_bounds(const double *verts, int64_t n, double out[6], void *stream);
+/* The engine's current positions as DEVICE float64 (N, 3), enqueued on the
+   engine's stream (cs_stream): the snapshot's cloth vertices without a
+   host round trip (bench.py:186 reads them back in the reference). */
+int cs_positions_device(cs_engine *h, double *dev_out);
+int cs_snapshot_render(const double *verts, const int32_t *tris, int64_t num_tris,
+                       int64_t num_cloth_tris, const double view[3], const int32_t axes[3],
+                       int32_t width, int32_t height, uint8_t *rgb, void *scratch, void *stream);
 const char *cs_last_error(void);
 int cs_abi_version(void);
 

@@ -35,6 +35,7 @@ from .mesh import (
     unique_edges,
 )
 from .scenes import ScenarioConfig, Scene, baseline_scene, build_scene, stable_coefficients
+from .snapshot import render_snapshot, snapshot_png
 
 __version__ = "0.1.0"
 
@@ -46,4 +47,5 @@ __all__ = [
     "compute_face_normals", "compute_vertex_normals", "generate_cloth_grid",
     "generate_icosphere", "generate_uv_sphere", "spring_count_formula", "unique_edges",
     "ScenarioConfig", "Scene", "baseline_scene", "build_scene", "stable_coefficients",
+    "render_snapshot", "snapshot_png",
 ]

@@ -127,6 +127,10 @@ SIGNATURES = {
     "cs_ipc_close": (_I32, [_P]),
     "cs_kernels_per_frame": (_I32, [_P, ctypes.POINTER(_I32)]),
     "cs_broadphase_stats": (_I32, [_P, ctypes.POINTER(_I64)]),
+    "cs_positions_device": (_I32, [_P, _P]),
+    "cs_snapshot_bounds": (_I32, [_P, _I64, ctypes.POINTER(ctypes.c_double), _P]),
+    "cs_snapshot_render": (_I32, [_P, _P, _I64, _I64, ctypes.POINTER(ctypes.c_double),
+                                  ctypes.POINTER(_I32), _I32, _I32, _P, _P, _P]),
     "cs_last_error": (ctypes.c_char_p, []),
     "cs_abi_version": (_I32, []),
     "cs_device_count": (_I32, []),

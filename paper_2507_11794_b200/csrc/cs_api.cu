@@ -192,6 +192,15 @@ __global__ void k_planes_to_aos(int64_t N, int64_t nx, int64_t pitch, int64_t pl
     const int64_t g = (n / nx) * pitch + (n % nx);
     for (int c = 0; c < comps; ++c) aos[n * comps + c] = planes[c * plane + g];
 }
+// positions (3 planes, f32 or f64) -> device f64 (N,3): the snapshot's input
+template <typename T>
+__global__ void k_planes_to_aos64(int64_t N, int64_t nx, int64_t pitch, int64_t plane,
+                                  const T *__restrict__ planes, double *__restrict__ aos) {
+    const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    const int64_t g = (n / nx) * pitch + (n % nx);
+    for (int c = 0; c < 3; ++c) aos[n * 3 + c] = (double)planes[c * plane + g];
+}
 __global__ void k_f64_to_f32(int64_t n, const double *a, float *b) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) b[i] = (float)a[i];
@@ -1287,4 +1296,53 @@ extern "C" int cs_mem_info(int64_t *free_bytes, int64_t *total_bytes) {
     if (free_bytes) *free_bytes = (int64_t)f;
     if (total_bytes) *total_bytes = (int64_t)t;
     return 0;
+}
+
+// ---- snapshot_png on the device (io.py:225-287), cs_snapshot.cu ----------------
+namespace cs {
+cudaError_t snapshot_bounds(const double *verts, int64_t n, double out[6], cudaStream_t st);
+cudaError_t snapshot_render(const double *verts, const int32_t *tris, int64_t nt, int64_t n_cloth,
+                            const double view[3], const int32_t axes[3], int width, int height,
+                            uint8_t *rgb, void *scratch, cudaStream_t st);
+}  // namespace cs
+
+extern "C" int cs_snapshot_bounds(const double *verts, int64_t n, double out[6], void *stream) {
+    if (!verts || n <= 0 || !out) return fail(CS_E_INVALID, "cs_snapshot_bounds: no vertices");
+    const cudaError_t e = cs::snapshot_bounds(verts, n, out, (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(CS_E_CUDA, cudaGetErrorString(e));
+    return CS_OK;
+}
+
+extern "C" int cs_snapshot_render(const double *verts, const int32_t *tris, int64_t num_tris,
+                                  int64_t num_cloth_tris, const double view[3],
+                                  const int32_t axes[3], int32_t width, int32_t height,
+                                  uint8_t *rgb, void *scratch, void *stream) {
+    if (!verts || (num_tris > 0 && !tris) || !view || !axes || !rgb || !scratch)
+        return fail(CS_E_INVALID, "cs_snapshot_render: null argument");
+    if (width < 8 || height < 8) return fail(CS_E_INVALID, "snapshot size too small");
+    for (int k = 0; k < 3; ++k)
+        if (axes[k] < 0 || axes[k] > 2) return fail(CS_E_INVALID, "snapshot axes must be 0..2");
+    const cudaError_t e = cs::snapshot_render(verts, tris, num_tris, num_cloth_tris, view, axes,
+                                              width, height, rgb, scratch, (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(CS_E_CUDA, cudaGetErrorString(e));
+    return CS_OK;
+}
+
+// Current positions as device float64 (N, 3) on the engine's stream: the
+// engine-side input of cs_snapshot_render (what bench.py:186 feeds
+// snapshot_png from read_positions().astype(float64), without the readback).
+extern "C" int cs_positions_device(cs_engine *h, double *dev_out) {
+    if (!h || !dev_out) return fail(CS_E_INVALID, "null argument");
+    if (h->banded) {
+        if (int r = halo_wait(h)) return r;
+    }
+    const int64_t nxx = h->grid ? h->nx : h->N;
+    if (h->fp64)
+        k_planes_to_aos64<double><<<nb(h->N), 256, 0, h->st>>>(
+            h->N, nxx, h->pitch, h->plane, (const double *)h->state[h->cur], dev_out);
+    else
+        k_planes_to_aos64<float><<<nb(h->N), 256, 0, h->st>>>(
+            h->N, nxx, h->pitch, h->plane, (const float *)h->state[h->cur], dev_out);
+    CK(cudaGetLastError());
+    return CS_OK;
 }

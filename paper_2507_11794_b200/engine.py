@@ -584,6 +584,21 @@ class Engine:
         if vel is not None:
             self._write(N.BUF_VELOCITIES64, np.asarray(vel, dtype=np.float64))
 
+    def render_snapshot(self, size=(320, 240), axis: str = "y", obstacle: bool = True) -> np.ndarray:
+        """uint8 (H, W, 3) pixels of the current frame's snapshot (io.py:225-287),
+        rendered from device memory: only the image crosses PCIe."""
+        from .snapshot import engine_snapshot
+
+        return engine_snapshot(self, size=size, axis=axis, obstacle=obstacle)
+
+    def snapshot_png(self, path, size=(320, 240), axis: str = "y", obstacle: bool = True) -> None:
+        """PNG of the current frame: the pixels of the reference's
+        snapshot_png(path, read_positions().astype(float64), mesh.triangles,
+        obstacle...) (bench.py:186-198), without the positions readback."""
+        from .snapshot import _save_png
+
+        _save_png(path, self.render_snapshot(size=size, axis=axis, obstacle=obstacle))
+
     def state_plane(self, which: int):
         """(device pointer, pitch) of plane `which` (x y z vx vy vz) of the
         current state -- zero-copy access for the row-band halo exchange."""
