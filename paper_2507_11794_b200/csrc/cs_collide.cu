@@ -608,6 +608,14 @@ __global__ void __launch_bounds__(256)
 k_respond(const CollideArgs A, float *__restrict__ pos, const uint32_t *__restrict__ pinbits,
           const float *__restrict__ inv_mass, int average, int end_of_frame) {
     const uint32_t n = *A.touched_n;
+    // blocks past the touched list have no item in the grid-stride loop and
+    // leave at once: only the `busy` ones take part in the last-block
+    // protocol below (block 0 always, so an empty frame is still closed).
+    // C3 touches ~15K of 100K nodes: 60 of the 391 blocks do the fence +
+    // counter atomic instead of all of them.
+    const uint32_t need = (n + blockDim.x - 1) / blockDim.x;
+    const uint32_t busy = need < gridDim.x ? (need ? need : 1u) : gridDim.x;
+    if (blockIdx.x >= busy) return;
     uint32_t moved = 0;
     for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
         const int64_t g = A.touched[q];
@@ -634,7 +642,7 @@ k_respond(const CollideArgs A, float *__restrict__ pos, const uint32_t *__restri
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
-        last = atomicAdd(A.blocks_done, 1u) == gridDim.x - 1;
+        last = atomicAdd(A.blocks_done, 1u) == busy - 1;
     }
     __syncthreads();
     if (last && threadIdx.x == 0) {
