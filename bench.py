@@ -123,6 +123,7 @@ def run_reference(args, scene, config_name):
     oracle port, since the reference is Python and cannot travel), all host
     threads, same workload/metric."""
     from oracle import oracle as O
+    from paper_2507_11794_b200.scenes import BASELINE_CONFIGS
 
     threads = O.max_threads()
     O.set_threads(threads)
@@ -152,9 +153,10 @@ def run_reference(args, scene, config_name):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "steps/s",
         "n_gpus": args.gpus, "steps": done, "warmup": args.warmup,
-        "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1000.0 / v, "higher_is_better": True,
+        "scaling": "strong" if args.gpus > 1 else "weak",  # as the b200 arm's line
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": config_name, "nodes": n_full},
+        "config": {"workload": f"{config_name}: {BASELINE_CONFIGS[config_name]}", "nodes": n_full},
         "node_updates_per_s": v * n_full,
         "cpu_baseline": {"value": v, "unit": "steps/s", "cores": threads, "kind": "port",
                          "sample": f"{done} steps of oracle/ (restated float64 solver.step), "
