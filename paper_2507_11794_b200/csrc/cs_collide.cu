@@ -619,16 +619,26 @@ k_respond(const CollideArgs A, float *__restrict__ pos, const uint32_t *__restri
     uint32_t moved = 0;
     for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
         const int64_t g = A.touched[q];
+        // every load of the node issued at once (one dependent round trip
+        // after the touched list instead of two)
         const int cnt = A.count[g];
         const bool pinned = inv_mass ? !(inv_mass[g] > 0.f) : ((pinbits[g >> 5] >> (g & 31)) & 1u);
+        int32_t raw[3];
+        float x[3], v[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            raw[d] = A.acc[d * A.plane + g];
+            x[d] = pos[d * A.plane + g];
+            v[d] = pos[(3 + d) * A.plane + g];
+        }
         if (cnt > 0 && !pinned) {
             ++moved;
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
-                float dv = decode_fixed(A.acc[d * A.plane + g], A.scale_d);
+                float dv = decode_fixed(raw[d], A.scale_d);
                 if (average) dv = fdiv(dv, (float)cnt);
-                pos[(3 + d) * A.plane + g] = fmul(pos[(3 + d) * A.plane + g], -0.5f);
-                pos[d * A.plane + g] = fadd(pos[d * A.plane + g], dv);
+                pos[(3 + d) * A.plane + g] = fmul(v[d], -0.5f);
+                pos[d * A.plane + g] = fadd(x[d], dv);
             }
         }
         A.acc[g] = 0;
