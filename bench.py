@@ -325,6 +325,7 @@ def c5_roofline(P, torch, stream, args):
     scene = P.baseline_scene("C5")
     n = scene.mesh.num_nodes
     eng = P.Engine(scene.mesh, params=scene.params, stream=stream.cuda_stream)
+    scene_params = scene.params
     del scene
     for _ in range(3):
         eng.step()
@@ -353,6 +354,8 @@ def c5_roofline(P, torch, stream, args):
     frame_gbs = frame_bytes / (frame_ms * 1e-3) / 1e9
     finite = bool(np.isfinite(eng.read_positions()[:: 4097]).all())
     eng.close()
+    projection = band_projection(P, torch, stream, scene_params=scene_params, k=k,
+                                 frame_ms=frame_ms)
     # the frame is ONE launch (k_pair3<NORMALS=1>): the dominant kernel
     return {"workload": "C5: 4096x4096 hanging cloth, 1 GPU", "nodes": n,
             "steps_per_s": 1000.0 / frame_ms, "frame_ms": frame_ms, "kernels_per_frame": kpf,
@@ -367,7 +370,40 @@ def c5_roofline(P, torch, stream, args):
                                 "achieved": 48 * n / (ms * 1e-3) / 1e9,
                                 "frac": 48 * n / (ms * 1e-3) / 1e9 / peak,
                                 "traffic": _traffic("C5")},
-            "finite": finite, "l2": "inputs (1.0 GB per frame) larger than L2"}
+            "finite": finite, "l2": "inputs (1.0 GB per frame) larger than L2",
+            "band_projection": projection}
+
+
+def band_projection(P, torch, stream, scene_params, k, frame_ms):
+    """Config 5 split in N row bands (bench.py --gpus N): one band's frame
+    (4096 x (4096/N + 4) rows incl. halos, the fused kernel) timed alone on
+    this GPU -- the compute part of an N-GPU frame.  The seam exchange (peer
+    stores of two rows each way inside the kernel + a stream flag handshake
+    per frame) is not in it, so the speed-up is a compute-only projection."""
+    from paper_2507_11794_b200.mesh import grid_band
+
+    out = []
+    for gpus in (2, 4, 8):
+        rows = 4096 // gpus + 4
+        band = grid_band(4096, 4096, 0, rows, total_mass=0.05 * 4096 * 4096, pinned_rows="first")
+        band.positions = np.stack([band.positions[:, 0], -band.positions[:, 2],
+                                   np.zeros(len(band.positions))], axis=1)
+        eng = P.Engine(band, params=scene_params, stream=stream.cuda_stream)
+        eng.step_frames(3)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        eng.step_frames(k)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / k
+        eng.close()
+        out.append({"gpus": gpus, "band_rows": rows, "band_frame_ms": ms,
+                    "projected_speedup": frame_ms / ms})
+    return {"bands": out,
+            "note": "compute only: one band's fused frame kernel timed alone on this GPU "
+                    "(rows incl. 2+2 halo rows); the per-frame seam exchange is not included"}
 
 
 def collision_bench(P, torch, args):
