@@ -223,7 +223,8 @@ def main():
         torch.cuda.synchronize()
         return [a.elapsed_time(b) for a, b in evs]
 
-    for _ in range(args.warmup):
+    # collision scenes are timed draped (>= 200 frames first)
+    for _ in range(args.warmup if scene.obstacle is None else max(args.warmup, 200)):
         eng.step()
     torch.cuda.synchronize()
     with ClockSampler(0) as clk:
