@@ -320,8 +320,17 @@ def run_banded_bench(args, metric, clock_sampler=None, peak=None):
     # one GPU per rank; with fewer devices than ranks (a functional run on a
     # single-GPU box) ranks share devices -- each rank is its own process and
     # CUDA context, which the flag handshake requires
-    dev = local % max(1, torch.cuda.device_count())
+    ndev = max(1, torch.cuda.device_count())
+    dev = local % ndev
     torch.cuda.set_device(dev)
+    if exchange == "p2p" and ndev > 1:
+        # peer stores need load/store access to the neighbours' GPUs (NVLink /
+        # NVSwitch); without it the bands exchange halos over NCCL instead
+        # (every rank evaluates the same machine-wide condition, so all pick
+        # the same mode)
+        pairs = [(r % ndev, (r + 1) % ndev) for r in range(world - 1)]
+        if not all(a == b or torch.cuda.can_device_access_peer(a, b) for a, b in pairs):
+            exchange = "nccl"
     if exchange == "nccl":
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     else:  # the data path is peer stores: the process group only swaps IPC handles
