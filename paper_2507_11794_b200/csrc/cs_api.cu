@@ -383,6 +383,11 @@ static void launch_frame(cs_engine *h) {
 // ---------------------------------------------------------------------------
 typedef CUresult (*PfnValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 static PfnValue32 g_wait32 = nullptr, g_write32 = nullptr;
+// CU_STREAM_WAIT_VALUE_FLUSH where the device supports it: remote (peer)
+// writes that reached this GPU before the flag are visible to the work the
+// wait releases -- the neighbour's halo stores, for the next pass
+static unsigned g_wait_flush = 0;
+typedef CUresult (*PfnDevAttr)(int *, CUdevice_attribute, CUdevice);
 
 static int load_memops() {
     if (g_wait32 && g_write32) return 0;
@@ -396,6 +401,15 @@ static int load_memops() {
         g_wait32 = g_write32 = nullptr;
         return fail(CS_E_CUDA, "the driver does not provide cuStreamWaitValue32/cuStreamWriteValue32");
     }
+    PfnDevAttr attr = nullptr;
+    cudaDriverEntryPointQueryResult q3 = cudaDriverEntryPointSymbolNotFound;
+    int dev = 0, flush = 0;
+    if (cudaGetDriverEntryPointByVersion("cuDeviceGetAttribute", (void **)&attr, 12000,
+                                         cudaEnableDefault, &q3) == cudaSuccess &&
+        q3 == cudaDriverEntryPointSuccess && attr && cudaGetDevice(&dev) == cudaSuccess &&
+        attr(&flush, CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES, (CUdevice)dev) == CUDA_SUCCESS &&
+        flush)
+        g_wait_flush = CU_STREAM_WAIT_VALUE_FLUSH;
     return 0;
 }
 
@@ -408,9 +422,11 @@ static int load_memops() {
 
 static int halo_wait(cs_engine *h) {
     if (h->up.on)
-        CU(g_wait32((CUstream)h->st, (CUdeviceptr)(h->hflags + 0), h->passes, CU_STREAM_WAIT_VALUE_GEQ));
+        CU(g_wait32((CUstream)h->st, (CUdeviceptr)(h->hflags + 0), h->passes,
+                    CU_STREAM_WAIT_VALUE_GEQ | g_wait_flush));
     if (h->dn.on)
-        CU(g_wait32((CUstream)h->st, (CUdeviceptr)(h->hflags + 1), h->passes, CU_STREAM_WAIT_VALUE_GEQ));
+        CU(g_wait32((CUstream)h->st, (CUdeviceptr)(h->hflags + 1), h->passes,
+                    CU_STREAM_WAIT_VALUE_GEQ | g_wait_flush));
     return 0;
 }
 
