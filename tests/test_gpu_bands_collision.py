@@ -213,3 +213,27 @@ def test_ipc_linked_bands_across_processes(n, world, obstacle):
         cmd.append(obstacle)
     res = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=280)
     assert res.returncode == 0 and "'ok'" in res.stdout, res.stdout + res.stderr[-2000:]
+
+
+def test_bench_gpus_2_under_torchrun_prints_one_banded_line():
+    """The driver's N > 1 launch of bench.py (torchrun, one process per
+    band, p2p halo stores + flag handshake) on this box -- functional only
+    (both ranks may share one GPU): rank 0 prints one JSON line for config
+    5 with the whole-job fields, and the sheet stays finite."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py", "--gpus", "2",
+           "--steps", "5", "--warmup", "3"]
+    res = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=280)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, res.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["config"]["nodes"] == 4096 * 4096 and d["finite"]
+    assert {"roofline", "e2e", "gpu_launches", "clocks"} <= set(d)
