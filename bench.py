@@ -426,8 +426,19 @@ def collision_bench(P, torch, args):
     ms = a.elapsed_time(b) / k
     st = eng.stats()
     pos = eng.read_positions()
+    n_nodes, n_tris = scene.mesh.num_nodes, len(scene.obstacle.triangles)
+    # compulsory bytes of a frame: the fused step's 60 B/node, the obstacle's
+    # corners + normals (48 B/triangle) read by detection, and the respond
+    # pass on the touched nodes (~40 B each); the grid is read sparsely
+    touched = st["responded"] if "responded" in st else 0
+    frame_bytes = 60 * n_nodes + 48 * n_tris + 40 * int(touched)
+    peak, _ = _peaks()
+    achieved = frame_bytes / (ms * 1e-3) / 1e9
     return {"workload": "C3: " + P.scenes.BASELINE_CONFIGS["C3"], "steps_per_s": 1000.0 / ms,
             "ms_per_step": ms, "node_updates_per_s": 1000.0 / ms * scene.mesh.num_nodes,
+            "roofline": {"bound": "latency (dependent grid lookups per query; SURVEY 8(d))",
+                         "bytes_per_frame": frame_bytes, "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak},
             "contacts_per_step": (st["hit_counter"] - hits_before) / k,
             "finite": bool(np.isfinite(pos).all()), "kernels_per_frame": eng.kernels_per_frame,
             "broadphase": eng.broadphase_stats()}
