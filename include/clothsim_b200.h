@@ -160,6 +160,11 @@ typedef struct cs_stats {
 #define CS_BUF_EXT_ACCEL 7      /* f32 (N,3) externalAccel (write only) */
 #define CS_BUF_POSITIONS64 8    /* f64 (N,3) (CS_FLAG_FP64 engines) */
 #define CS_BUF_VELOCITIES64 9
+#define CS_BUF_NORMALS_LAGGED 10 /* f32 (N,3) the normals the last fused step
+                                    kernel produced -- those of the PREVIOUS
+                                    frame's final state -- without the
+                                    recompute CS_BUF_NORMALS does (a renderer
+                                    that accepts a one-frame lag pays nothing) */
 
 /* passes for cs_run_pass (engine.py:313-339) */
 #define CS_PASS_FORCE_INTEGRATE 0 /* zero_forces + spring_force + integrate */

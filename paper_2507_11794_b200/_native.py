@@ -35,6 +35,7 @@ FLAG_WARP_NARROW = 2048
 BUF_POSITIONS, BUF_VELOCITIES, BUF_NORMALS, BUF_PREV_POSITIONS = 0, 1, 2, 3
 BUF_FORCES_RAW, BUF_ACCUMULATOR, BUF_COUNTS, BUF_EXT_ACCEL = 4, 5, 6, 7
 BUF_POSITIONS64, BUF_VELOCITIES64 = 8, 9
+BUF_NORMALS_LAGGED = 10
 
 PASS_FORCE_INTEGRATE, PASS_DETECT, PASS_RESPOND, PASS_NORMALS = 0, 1, 2, 3
 

@@ -1053,12 +1053,13 @@ extern "C" int cs_read(cs_engine *h, int32_t id, void *dst) {
         case CS_BUF_POSITIONS:
         case CS_BUF_VELOCITIES:
         case CS_BUF_PREV_POSITIONS:
-        case CS_BUF_NORMALS: {
+        case CS_BUF_NORMALS:
+        case CS_BUF_NORMALS_LAGGED: {
             if (id == CS_BUF_NORMALS) flush_normals(h);
             if (h->banded) {
                 if (int r = halo_wait(h)) return r;  // halo rows of the current state landed
             }
-            const void *base = id == CS_BUF_NORMALS ? h->normals
+            const void *base = (id == CS_BUF_NORMALS || id == CS_BUF_NORMALS_LAGGED) ? h->normals
                                : id == CS_BUF_PREV_POSITIONS ? h->state[1 - h->cur]
                                                              : h->state[h->cur];
             const int64_t o = id == CS_BUF_VELOCITIES ? 3 * P : 0;

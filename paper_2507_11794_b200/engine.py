@@ -551,6 +551,12 @@ class Engine:
     def read_normals(self, out=None) -> np.ndarray:
         return self._read(N.BUF_NORMALS, _F32, 3, out)
 
+    def read_normals_lagged(self, out=None) -> np.ndarray:
+        """The normals the last fused step kernel produced: those of the
+        previous frame's final state (a one-frame lag), read without the
+        stand-alone recompute read_normals() does for the current state."""
+        return self._read(N.BUF_NORMALS_LAGGED, _F32, 3, out)
+
     def read_previous_positions(self) -> np.ndarray:
         return self._read(N.BUF_PREV_POSITIONS, _F32, 3)
 

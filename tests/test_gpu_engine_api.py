@@ -222,3 +222,22 @@ def test_run_frames_stats_rows(tmp_path):
         sum(eng._frame_hits(f)[0] for f in range(100))
     F.write_stats_csv(tmp_path / "s.csv", rows)
     assert len(F.parse_stats_csv(tmp_path / "s.csv")) == 20
+
+
+@pytest.mark.parametrize("scene", ["hanging", "drop"])
+def test_lagged_normals_are_the_previous_frames_normals(scene):
+    """The fused step kernel computes frame t's normals during frame t+1
+    (after frame t's respond pass); read_normals_lagged() returns them
+    without a recompute, bit-identical to what read_normals() gave one frame
+    earlier on an engine that runs the normals pass at the end of each frame
+    (normals="split", the reference's pass order)."""
+    if scene == "hanging":
+        sc = P.build_scene(P.ScenarioConfig("hanging", (67, 45), dt=0.004))
+    else:
+        sc = P.build_scene(P.ScenarioConfig("drop", (24, 24), obstacle="icosphere:2"))
+    fused = P.Engine(sc.mesh, sc.obstacle, sc.params, pair_budget=10**12)
+    split = P.Engine(sc.mesh, sc.obstacle, sc.params, pair_budget=10**12, normals="split")
+    fused.step_frames(40)
+    split.step_frames(39)
+    np.testing.assert_array_equal(fused.read_normals_lagged(), split.read_normals())
+    np.testing.assert_array_equal(fused.read_previous_positions(), split.read_positions())
