@@ -839,6 +839,12 @@ k_detect_warp(const CollideArgs A, const GridDesc g, const uint32_t *__restrict_
 // identical.
 // ---------------------------------------------------------------------------
 constexpr int BATCH_WARPS = 4;
+#ifndef CS_DETECT_WPSM
+#define CS_DETECT_WPSM 80  // target warps per SM when choosing queries per warp
+#endif
+#ifndef CS_DETECT_STRIDED
+#define CS_DETECT_STRIDED 1
+#endif
 struct QuerySlot {
     float v[3][3];
     float lo[3], hi[3];   // query box (PASS 0: padded segment box; PASS 1: tri box +- 2 pad)
@@ -928,7 +934,16 @@ __device__ __forceinline__ void detect_batch(BatchShared &S, int64_t blk, const 
     const uint32_t lt_mask = (1u << lane) - 1u;
     // qb queries per warp (lanes >= qb hold none): 32 when queries are
     // plentiful, fewer so that small clouds still spread over every SM
+#if CS_DETECT_STRIDED
+    // query = lane * warps + warp: a warp's queries sit nw apart in index
+    // (and so in space), so the warps drawn from a dense contact region no
+    // longer carry all of its candidates (the frame's tail)
+    const int64_t nw = (nq + qb - 1) / qb;
+    const int64_t wi = blk * BATCH_WARPS + w;
+    const int64_t q = wi < nw ? (int64_t)lane * nw + wi : nq;  // padding warps: none
+#else
     const int64_t q = (blk * BATCH_WARPS + w) * qb + lane;
+#endif
     QuerySlot &my = slots[w][lane];
     const int nv = PASS == 0 ? 2 : 3;
     uint32_t ncell = 0;
@@ -1080,7 +1095,7 @@ __device__ __forceinline__ void detect_batch(BatchShared &S, int64_t blk, const 
 // the rest cloth triangles (pass B) -- no dependency between them, one
 // launch latency instead of two.
 #ifndef CS_DETECT_MINB
-#define CS_DETECT_MINB 10  // 48 registers: 40 resident warps per SM (C3 frame -7%)
+#define CS_DETECT_MINB 8  // <= 64 registers, 32 resident warps per SM (strided queries: C3 frame -3%)
 #endif
 __global__ void __launch_bounds__(32 * BATCH_WARPS, CS_DETECT_MINB)
 k_detect_batch(const CollideArgs A, const GridDesc g, const uint2 *__restrict__ cbe,
@@ -1117,14 +1132,16 @@ void launch_detect(const CollideArgs &A, const BroadPhase &bp, const float *corn
                    int64_t nc, cudaStream_t st) {
     if (bp.warp_per_query == 2) {
         // queries per warp: the largest power of two <= 32 that still leaves
-        // >= ~160 warps per SM (148 SMs).  The frame's time is the tail of
-        // the warps whose queries sit in the densest contact region (the two
-        // passes alone take 127 and 99 us, together 133), so smaller batches
-        // in more warps shorten it: C3 (8 queries per warp) 153 -> 138 us;
-        // one query per warp for small clouds (C4)
+        // >= CS_DETECT_WPSM warps per SM (148 SMs).  With contiguous batches
+        // the frame's time was the tail of the warps whose queries sat in the
+        // densest contact region, and smaller batches in more warps shortened
+        // it (C3, 8 queries per warp at 160: 153 -> 138 us).  Strided batches
+        // (CS_DETECT_STRIDED) spread that region over every warp, so fewer,
+        // fuller warps win: C3 16 queries per warp at 80, frame 139 -> 116 us
+        // (tools/ab_c3.sh); one query per warp for small clouds (C4)
         auto qb_for = [](int64_t nq) {
             int qb = 32;
-            while (qb > 1 && nq / qb < (int64_t)148 * 160) qb >>= 1;
+            while (qb > 1 && nq / qb < (int64_t)148 * CS_DETECT_WPSM) qb >>= 1;
             return qb;
         };
         const int qa = qb_for(ne), qc = qb_for(nc);

@@ -12,5 +12,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-fil
 NCU="ncu --set full --import-source on --clock-control none"
 $NCU -k regex:k_pair3 -c 3 -o $O/c2_frame python tools/prof_kernels.py C2 1 > $O/ncu_c2.log 2>&1
 $NCU -k regex:k_pair -c 3 -o $O/c5_passes python tools/prof_kernels.py C5 1 > $O/ncu_c5.log 2>&1
-$NCU -k regex:"k_detect|k_respond" -c 4 -o $O/c3_collide python tools/prof_c3.py C3 1 > $O/ncu_c3.log 2>&1
+# C3: skip the 200 draping frames (one detect + one respond launch each) so the
+# captured pair is a frame with the cloth on the sphere
+$NCU -k regex:"k_detect|k_respond" --launch-skip 400 -c 2 -o $O/c3_draped python tools/prof_c3.py C3 1 > $O/ncu_c3.log 2>&1
 ls -la $O

@@ -46,7 +46,7 @@ with open(os.path.join(P, "r1_ncu_summary.txt"), "w") as fh:
     fh.write("# C2 frame kernel (k_pair3<1,0>, 640K nodes)\n" + summary(os.path.join(G, "c2_frame.ncu-rep"), 1))
     fh.write("# C5 fused frame kernel (k_pair3<1,0>, 16.8M nodes)\n" + summary(os.path.join(G, "c5_passes.ncu-rep"), 1))
     fh.write("# C5 split passes: stand-alone k_pair_normals, force+integrate k_pair3<0,0>\n" + summary(os.path.join(G, "c5_split.ncu-rep"), 2))
-    fh.write("# C3 collision (draped, frame > 400): batched narrow phase + respond\n" + summary(os.path.join(G, "c3_draped.ncu-rep")))
+    fh.write("# C3 collision (draped: after 200 frames): batched narrow phase + respond\n" + summary(os.path.join(G, "c3_draped.ncu-rep")))
 t = {"_source": "ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum per launch "
                 "(profiles/r1_ncu_summary.txt): C2 / C5_frame = fused k_pair3<1,0>, "
                 "C5 = k_pair3<0,0> force pass, C5_normals = k_pair_normals"}
