@@ -838,7 +838,10 @@ k_detect_warp(const CollideArgs A, const GridDesc g, const uint32_t *__restrict_
 // other two mappings, so the hit set and the integer accumulators are
 // identical.
 // ---------------------------------------------------------------------------
-constexpr int BATCH_WARPS = 4;
+#ifndef CS_DETECT_BATCH_WARPS
+#define CS_DETECT_BATCH_WARPS 4
+#endif
+constexpr int BATCH_WARPS = CS_DETECT_BATCH_WARPS;  // warps per narrow-phase block
 #ifndef CS_DETECT_WPSM
 #define CS_DETECT_WPSM 80  // target warps per SM when choosing queries per warp
 #endif
