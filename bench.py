@@ -44,6 +44,9 @@ sys.path.insert(0, ROOT)
 METRIC = "sim steps/s & node-updates/s: 640K-node cloth; 100K cloth vs 100K-tri collision"
 
 
+SLOWDOWN_REASONS = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -227,20 +230,26 @@ def main():
     for _ in range(args.warmup if scene.obstacle is None else max(args.warmup, 200)):
         eng.step()
     torch.cuda.synchronize()
-    with ClockSampler(0) as clk:
-        # one frame = ONE kernel launch (fused force + integrate + the
-        # previous frame's normals), so the per-step events time that kernel
-        times = timed_steps(args.steps)
-        # L2-resident steady state (the state stays on chip frame to frame)
-        torch.cuda.synchronize()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        eng.step_frames(args.steps)
-        b.record(stream)
-        torch.cuda.synchronize()
-        warm_ms = a.elapsed_time(b) / args.steps
-        big = c5_roofline(P, torch, stream, args) if not args.no_c5 else None
+    # a timed region that saw a hardware / thermal slowdown is measured once more
+    for attempt in range(2):
+        with ClockSampler(0) as clk:
+            # one frame = ONE kernel launch (fused force + integrate + the
+            # previous frame's normals), so the per-step events time that kernel
+            times = timed_steps(args.steps)
+            # L2-resident steady state (the state stays on chip frame to frame)
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            eng.step_frames(args.steps)
+            b.record(stream)
+            torch.cuda.synchronize()
+            warm_ms = a.elapsed_time(b) / args.steps
+            big = c5_roofline(P, torch, stream, args) if not args.no_c5 else None
+        throttled = sorted(set(clk.summary()["reasons"]) & SLOWDOWN_REASONS)
+        if not throttled:
+            break
+        print(f"bench: the timed region saw {throttled}; measuring once more", file=sys.stderr)
     ms = float(np.sum(times)) / args.steps
     value = 1000.0 / ms
     peak, peak_src = _peaks()
@@ -296,7 +305,7 @@ def main():
                              "figure is roofline_c5"},
         "roofline_c5": big,
         "gpu_launches": kpf * args.steps,
-        "clocks": clk.summary(),
+        "clocks": dict(clk.summary(), remeasured=attempt),
         "e2e": e2e,
     }
     if not args.no_collision and config_name == "C2":
