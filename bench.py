@@ -15,15 +15,21 @@ vertex normals.  Synthetic inputs (the reference's own scene builder).
                initial state uploaded from pinned memory inside the timed
                region, every step reads the positions back (D2H) -- what a
                renderer consumes.
-* roofline     the fused force+integrate kernel alone, CUDA-event timed
-               (L2 flushed), algorithmic 48 B/node vs MEASURED_PEAKS hbm_gbs.
+* roofline     the frame's one kernel (k_pair3<NORMALS=1>: spring force +
+               integrate + the previous frame's normals), CUDA-event timed
+               with L2 flushed, algorithmic 60 B/node (24 B read, 24 B + 12 B
+               normals written) vs MEASURED_PEAKS hbm_gbs; roofline_c5 gives
+               the same at C5 (1.0 GB/frame, HBM-bound) plus the force-only
+               pass (48 B/node).
 * cpu_baseline the CPU oracle (restatement of the reference float64 solver,
                oracle/) on this host's cores, bounded sample of the workload.
 * collision    config 3 (316x316 vs the 99,904-triangle sphere) steps/s after
                a 200-frame drape.
 
 N>1 (torchrun): config 5 (4096^2) row-band partitioned, 2-row halos
-exchanged over NCCL each step; value = whole-job steps/s (strong scaling).
+stored into the neighbours by the step kernel itself (peer memory through
+CUDA IPC over NVLink, stream-ordered flag handshake; NCCL send/recv only when
+peer access is missing); value = whole-job steps/s (strong scaling).
 """
 
 from __future__ import annotations
@@ -56,15 +62,28 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def smi_gpu_id(dev=0):
+    """nvidia-smi's name for CUDA device `dev`: its UUID (nvidia-smi ignores
+    CUDA_VISIBLE_DEVICES and may number GPUs differently from CUDA)."""
+    try:
+        import torch
+
+        u = str(torch.cuda.get_device_properties(dev).uuid)
+        return u if u.startswith("GPU-") else "GPU-" + u
+    except Exception:
+        return str(dev)
+
+
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region,
+    on the GPU the CUDA device `dev` is (selected by UUID)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index=0):
-        self.index, self.samples, self._stop = index, [], threading.Event()
+    def __init__(self, dev=0):
+        self.index, self.samples, self._stop = smi_gpu_id(dev), [], threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
@@ -230,7 +249,9 @@ def main():
     for _ in range(args.warmup if scene.obstacle is None else max(args.warmup, 200)):
         eng.step()
     torch.cuda.synchronize()
-    # a timed region that saw a hardware / thermal slowdown is measured once more
+    # a timed region that saw a hardware / thermal slowdown is measured once
+    # more; both attempts stay in the line
+    attempts = []
     for attempt in range(2):
         with ClockSampler(0) as clk:
             # one frame = ONE kernel launch (fused force + integrate + the
@@ -247,6 +268,8 @@ def main():
             warm_ms = a.elapsed_time(b) / args.steps
             big = c5_roofline(P, torch, stream, args) if not args.no_c5 else None
         throttled = sorted(set(clk.summary()["reasons"]) & SLOWDOWN_REASONS)
+        attempts.append({"ms_per_step": float(np.sum(times)) / args.steps,
+                         "clocks": clk.summary()})
         if not throttled:
             break
         print(f"bench: the timed region saw {throttled}; measuring once more", file=sys.stderr)
@@ -306,6 +329,7 @@ def main():
         "roofline_c5": big,
         "gpu_launches": kpf * args.steps,
         "clocks": dict(clk.summary(), remeasured=attempt),
+        "attempts": attempts,
         "e2e": e2e,
     }
     if not args.no_collision and config_name == "C2":
@@ -348,7 +372,10 @@ def c5_roofline(P, torch, stream, args):
     b.record(stream)
     torch.cuda.synchronize()
     frame_ms = a.elapsed_time(b) / k
-    # the force + integrate pass alone (k_pair3<NORMALS=0>, 48 B/node)
+    # the force + integrate pass alone (k_pair3<NORMALS=0>, 48 B/node); one
+    # untimed pass first: it refreshes the fused path's stale normals, so no
+    # stand-alone normals launch lands inside a timed sample
+    P._native.check(eng._lib.cs_run_pass(eng._handle, P._native.PASS_FORCE_INTEGRATE))
     evs = []
     for _ in range(k):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

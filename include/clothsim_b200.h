@@ -249,6 +249,15 @@ int cs_ipc_close(void *dev_ptr);
 int cs_kernels_per_frame(cs_engine *h, int32_t *count);
 /* Broad-phase statistics: cells, references, last frame's candidate pairs. */
 int cs_broadphase_stats(cs_engine *h, int64_t out[4]);
+/* The broad-phase grid itself, for the bit-exact grid-cell assignment
+   check (north star; the reference brute-forces every pair, its prefilter
+   test test_gpu_engine.py:267-307 is the contract): geometry[8] = origin
+   xyz, 1/cell, cell edge (f32, rest 0); dims[3] = cells per axis; the sorted
+   (cell key, triangle) references, cs_broadphase_stats out[1] of each; per
+   cell [begin, end) into them, out[0] of each (0, 0 for an empty cell).
+   Any output may be NULL.  Synchronises. */
+int cs_broadphase_dump(cs_engine *h, float geometry[8], int32_t dims[3], uint32_t *ref_keys,
+                       uint32_t *ref_tris, uint32_t *cell_begin, uint32_t *cell_end);
 /* Number of visible CUDA devices (0 when no driver / device): the adapter
    probe of gpu/device.py:156-172 get_adapter. */
 int cs_device_count(void);

@@ -406,6 +406,86 @@ def boundary_distance(start, end, v0, v1, v2, eps=1e-6):
     return min(m)
 
 
+# ---------------------------------------------------------------------------
+# Broad-phase grid (no reference counterpart: the reference brute-forces every
+# pair, collision.py:243-315 / kernels.py:186-290, and its own test pins a
+# prefilter to brute force, test_gpu_engine.py:267-307).  A numpy float32
+# restatement of the device build in csrc/cs_collide.cu build_broadphase, so
+# the north star's "bit-exact grid-cell assignment" has a checker.
+# ---------------------------------------------------------------------------
+
+def grid_geometry(corners, cell_size=None):
+    """(origin f32[3], inv_cell f32, cell f32, dims int[3]) of the uniform grid
+    over the obstacle's triangle boxes: origin = min corner of the union box;
+    cell edge = f32(mean over triangles of the largest box extent), summed in
+    float64 in triangle order (or `cell_size`); dims[d] = ceil((hi-lo)/cell)+1,
+    the edge grown x1.25 (f32) until the grid has at most 2^24 cells."""
+    c = np.asarray(corners, dtype=np.float32).reshape(-1, 3, 3)
+    lo = np.minimum(np.minimum(c[:, 0], c[:, 1]), c[:, 2])
+    hi = np.maximum(np.maximum(c[:, 0], c[:, 1]), c[:, 2])
+    glo, ghi = lo.min(axis=0), hi.max(axis=0)
+    ext = (hi - lo).max(axis=1).astype(np.float64)
+    mean = float(np.add.accumulate(ext)[-1]) / max(len(c), 1)  # sequential f64 sum
+    cell = np.float32(cell_size) if cell_size else np.float32(mean)
+    if not cell > 0:
+        cell = np.float32(1.0)
+    while True:
+        dims = [max(1, int(math.ceil(float(ghi[d] - glo[d]) / float(cell))) + 1) for d in range(3)]
+        if dims[0] * dims[1] * dims[2] <= (1 << 24):
+            break
+        cell = np.float32(cell * np.float32(1.25))
+    return glo, np.float32(np.float32(1.0) / cell), cell, dims
+
+
+def grid_cell_of(x, origin, inv_cell, dims):
+    """cell_of per axis: floor(f32(f32(x - origin) * inv_cell)), clamped to
+    [0, dims-1] (NaN -> 0); x is (..., 3) float32."""
+    f = np.floor((np.asarray(x, np.float32) - origin) * inv_cell)
+    out = np.zeros(f.shape, dtype=np.int64)
+    for d in range(3):
+        fd = f[..., d]
+        v = np.where(fd >= 0, fd, 0.0)
+        v = np.where(v >= dims[d] - 1, dims[d] - 1, v)
+        out[..., d] = v.astype(np.int64)
+    return out
+
+
+def broadphase_grid(corners, cell_size=None):
+    """The grid-cell assignment: every triangle is referenced by each cell its
+    (unpadded) box covers, cells enumerated z-major then y then x, and the
+    (cell key, triangle) references sorted stably by key (key = (z*dy + y)*dx
+    + x).  Returns dict(origin, inv_cell, cell, dims, ref_keys, ref_tris,
+    cell_begin, cell_end) -- empty cells have begin = end = 0."""
+    c = np.asarray(corners, dtype=np.float32).reshape(-1, 3, 3)
+    origin, inv_cell, cell, dims = grid_geometry(c, cell_size)
+    lo = np.minimum(np.minimum(c[:, 0], c[:, 1]), c[:, 2])
+    hi = np.maximum(np.maximum(c[:, 0], c[:, 1]), c[:, 2])
+    a = grid_cell_of(lo, origin, inv_cell, dims)
+    b = grid_cell_of(hi, origin, inv_cell, dims)
+    w = b - a + 1
+    counts = w[:, 0] * w[:, 1] * w[:, 2]
+    tri = np.repeat(np.arange(len(c), dtype=np.int64), counts)
+    start = np.concatenate([[0], np.cumsum(counts)[:-1]])
+    q = np.arange(int(counts.sum()), dtype=np.int64) - np.repeat(start, counts)
+    wx, wy = w[tri, 0], w[tri, 1]
+    x = a[tri, 0] + q % wx
+    y = a[tri, 1] + (q // wx) % wy
+    z = a[tri, 2] + q // (wx * wy)
+    keys = (z * dims[1] + y) * dims[0] + x
+    order = np.argsort(keys, kind="stable")
+    keys, tris = keys[order].astype(np.uint32), tri[order].astype(np.uint32)
+    ncell = dims[0] * dims[1] * dims[2]
+    beg = np.zeros(ncell, dtype=np.uint32)
+    end = np.zeros(ncell, dtype=np.uint32)
+    if len(keys):
+        first = np.flatnonzero(np.r_[True, keys[1:] != keys[:-1]])
+        last = np.r_[first[1:], len(keys)]
+        beg[keys[first]] = first
+        end[keys[first]] = last
+    return {"origin": origin, "inv_cell": inv_cell, "cell": cell, "dims": tuple(dims),
+            "ref_keys": keys, "ref_tris": tris, "cell_begin": beg, "cell_end": end}
+
+
 def encode(x, scale=1 << 16):
     return int(lib().or_encode(float(np.float32(x)), float(np.float32(scale))))
 

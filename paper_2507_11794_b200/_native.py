@@ -128,6 +128,8 @@ SIGNATURES = {
     "cs_ipc_close": (_I32, [_P]),
     "cs_kernels_per_frame": (_I32, [_P, ctypes.POINTER(_I32)]),
     "cs_broadphase_stats": (_I32, [_P, ctypes.POINTER(_I64)]),
+    "cs_broadphase_dump": (_I32, [_P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(_I32), _P,
+                                  _P, _P, _P]),
     "cs_positions_device": (_I32, [_P, _P]),
     "cs_snapshot_bounds": (_I32, [_P, _I64, ctypes.POINTER(ctypes.c_double), _P]),
     "cs_snapshot_render": (_I32, [_P, _P, _I64, _I64, ctypes.POINTER(ctypes.c_double),

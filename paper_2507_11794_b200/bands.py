@@ -352,6 +352,7 @@ def run_banded_bench(args, metric, clock_sampler=None, peak=None):
     torch.cuda.synchronize()
     dist.barrier()
     slowdowns = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    attempts = []
     for attempt in range(2):  # a throttled timed region is measured once more
         sampler = clock_sampler(dev) if (clock_sampler and rank == 0) else contextlib.nullcontext()
         with sampler as clk:
@@ -363,8 +364,11 @@ def run_banded_bench(args, metric, clock_sampler=None, peak=None):
             torch.cuda.synchronize()
         dist.barrier()
         again = torch.zeros(1, dtype=torch.float64, device=red_dev)
-        if clock_sampler and rank == 0 and set(clk.summary()["reasons"]) & slowdowns:
-            again[0] = 1.0
+        if clock_sampler and rank == 0:
+            attempts.append({"rank0_ms_per_step": a.elapsed_time(b) / args.steps,
+                             "clocks": clk.summary()})
+            if set(clk.summary()["reasons"]) & slowdowns:
+                again[0] = 1.0
         dist.broadcast(again, src=0)
         if attempt == 1 or not again.item():
             break
@@ -390,7 +394,16 @@ def run_banded_bench(args, metric, clock_sampler=None, peak=None):
     t0 = time.perf_counter()
     band.engine.write_positions(host_pos)
     band.engine.write_velocities(host_vel)
-    band.engine.simulate(k_e2e, out=traj)
+    if exchange == "p2p":
+        # the halo exchange travels inside the step kernels: simulate()
+        # streams every frame's positions while the next frame computes
+        band.engine.simulate(k_e2e, out=traj)
+    else:
+        # NCCL exchange: the engine alone would step stale halos, so each
+        # frame is the band's step + halo swap, then its positions D2H
+        for f in range(k_e2e):
+            band.step(1)
+            band.engine.read_positions(out=traj[f])
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     del traj
 
@@ -421,7 +434,10 @@ def run_banded_bench(args, metric, clock_sampler=None, peak=None):
                          "launch_ms": ms},
             "e2e": {"value": k_e2e / e2e_s, "unit": "steps/s",
                     "h2d_bytes_per_step": int(24 * n * n / k_e2e), "d2h_bytes_per_step": 12 * n * n,
-                    "api": "Engine.write_positions/write_velocities + Engine.simulate per band",
+                    "api": ("Engine.write_positions/write_velocities + Engine.simulate per band"
+                            if exchange == "p2p" else
+                            "Engine.write_positions/write_velocities + per frame BandedEngine.step "
+                            "(step + NCCL halo swap) + Engine.read_positions"),
                     "frames": k_e2e},
             "gpu_launches": args.steps * band.engine.kernels_per_frame * world,
             "finite": finite,
@@ -429,6 +445,7 @@ def run_banded_bench(args, metric, clock_sampler=None, peak=None):
         }
         if clock_sampler:
             line["clocks"] = dict(clk.summary(), remeasured=attempt)
+            line["attempts"] = attempts
         if torch.cuda.device_count() < world:
             line["note"] = (f"{world} ranks shared {torch.cuda.device_count()} GPU(s): a "
                             "functional run, not a scaling measurement")

@@ -913,6 +913,10 @@ extern "C" int cs_record(cs_engine *h, int32_t frames, float *host_out) {
         const int k = f & 1;
         if (f > 0) CK(cudaStreamWaitEvent(h->st, h->ev_moved[k ^ 1], 0));  // f-1 transposed
         if (int r = cs_step(h, 1)) return r;
+        // a row band's halo rows of the new state are the neighbours' peer
+        // stores: wait for their pass, as cs_read does, before copying
+        if (h->banded)
+            if (int r = halo_wait(h)) return r;
         CK(cudaEventRecord(h->ev_frame[k], h->st));
         CK(cudaStreamWaitEvent(h->copy_st, h->ev_frame[k], 0));
         k_planes_to_aos<float><<<nb(h->N), 256, 0, h->copy_st>>>(
@@ -1087,7 +1091,10 @@ extern "C" int cs_read(cs_engine *h, int32_t id, void *dst) {
             }
             if (!h->forces_raw) CK(dalloc(&h->forces_raw, 3 * P));
             const float *prev = (const float *)h->state[1 - h->cur];
-            if (h->grid)
+            if (h->grid && h->strip && !h->fixed && (h->flags & CS_FLAG_PAIRED))
+                // the fast kernel's own forces (k_pair3 in its read-only mode)
+                launch_pair3_forces(h->sp, prev, h->pinbits, h->forces_raw, h->st);
+            else if (h->grid)
                 launch_grid_forces(h->sp, prev, h->forces_raw, h->st);
             else
                 launch_csr_forces(h->cp, prev, h->csr_off, h->csr_nbr, h->csr_kind, h->csr_rest,
@@ -1296,6 +1303,30 @@ extern "C" int cs_broadphase_stats(cs_engine *h, int64_t out[4]) {
     out[1] = h->bp.num_refs;
     out[2] = h->bp.grid.dims[0];
     out[3] = h->bp.grid.dims[1] * (int64_t)h->bp.grid.dims[2];
+    return 0;
+}
+
+extern "C" int cs_broadphase_dump(cs_engine *h, float geometry[8], int32_t dims[3],
+                                  uint32_t *ref_keys, uint32_t *ref_tris, uint32_t *cell_begin,
+                                  uint32_t *cell_end) {
+    if (!h) return fail(CS_E_INVALID, "null engine");
+    if (!h->has_obstacle) return fail(CS_E_INVALID, "the engine has no obstacle (no broad phase)");
+    const GridDesc &g = h->bp.grid;
+    if (geometry) {
+        for (int d = 0; d < 3; ++d) geometry[d] = g.origin[d];
+        geometry[3] = g.inv_cell;
+        geometry[4] = g.cell;
+        geometry[5] = geometry[6] = geometry[7] = 0.f;
+    }
+    if (dims)
+        for (int d = 0; d < 3; ++d) dims[d] = g.dims[d];
+    CK(cudaStreamSynchronize(h->st));
+    const size_t R = (size_t)h->bp.num_refs * sizeof(uint32_t);
+    const size_t C = (size_t)h->bp.num_cells * sizeof(uint32_t);
+    if (ref_keys && R) CK(cudaMemcpy(ref_keys, h->bp.cell_keys, R, cudaMemcpyDeviceToHost));
+    if (ref_tris && R) CK(cudaMemcpy(ref_tris, h->bp.cell_tris, R, cudaMemcpyDeviceToHost));
+    if (cell_begin && C) CK(cudaMemcpy(cell_begin, h->bp.cell_begin, C, cudaMemcpyDeviceToHost));
+    if (cell_end && C) CK(cudaMemcpy(cell_end, h->bp.cell_end, C, cudaMemcpyDeviceToHost));
     return 0;
 }
 

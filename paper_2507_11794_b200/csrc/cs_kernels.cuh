@@ -187,6 +187,8 @@ void launch_push_rows(const float *src, int64_t plane, int pitch, int r0, int r1
                       float *const to[6], cudaStream_t st);
 void launch_pair_normals(const StepParams &p, const float *state, float *nrm, cudaStream_t st);
 int pair3_rows(const StepParams &p);
+void launch_pair3_forces(const StepParams &p, const float *src, const uint32_t *pinbits,
+                         int32_t *forces, cudaStream_t st);
 void launch_grid_forces(const StepParams &p, const float *src, int32_t *forces, cudaStream_t st);
 void launch_grid_normals(const StepParams &p, bool exact, const float *state, float *nrm,
                          cudaStream_t st);

@@ -136,10 +136,20 @@ class _StateView:
     """numpy-like read/write view of one (N,3) device buffer, so reference
     code such as ``eng.buffers.vel[0] = (0, 0, 2)`` keeps working."""
 
+    # a float64 engine's state goes through its f64 buffers, so writing one
+    # node leaves every other node's f64 value untouched (a round trip
+    # through the f32 buffers would round them all)
+    _F64 = {N.BUF_POSITIONS: N.BUF_POSITIONS64, N.BUF_VELOCITIES: N.BUF_VELOCITIES64}
+
     def __init__(self, engine, read_id, write_id):
         self._e, self._r, self._w = engine, read_id, write_id
 
+    def _wide(self, buf):
+        return self._e.precision == "fp64" and buf in self._F64
+
     def _get(self):
+        if self._wide(self._r):
+            return self._e._read(self._F64[self._r], np.float64, 3)
         return self._e._read(self._r, np.float32, 3)
 
     def __array__(self, dtype=None, copy=None):
@@ -154,13 +164,18 @@ class _StateView:
             raise TypeError("this buffer is read-only")
         a = self._get()
         a[idx] = value
-        self._e._write(self._w, a.astype(np.float32))
+        if self._wide(self._w):
+            self._e._write(self._F64[self._w], a)
+        else:
+            self._e._write(self._w, a.astype(np.float32))
 
     @property
     def shape(self):
         return (self._e.num_nodes, 3)
 
-    dtype = np.dtype(np.float32)
+    @property
+    def dtype(self):
+        return np.dtype(np.float64 if self._wide(self._r) else np.float32)
 
     def copy(self):
         return self._get()
@@ -415,6 +430,23 @@ class Engine:
         a = (ctypes.c_int64 * 4)()
         N.check(self._lib.cs_broadphase_stats(self._handle, a))
         return {"cells": a[0], "refs": a[1], "dims_x": a[2], "dims_yz": a[3]}
+
+    def broadphase_dump(self) -> dict:
+        """The device-built broad-phase grid (cs_broadphase_dump): origin,
+        1/cell, cell edge (f32), dims, the sorted (cell key, triangle)
+        references and each cell's [begin, end) into them."""
+        st = self.broadphase_stats()
+        geo = (ctypes.c_float * 8)()
+        dims = (ctypes.c_int32 * 3)()
+        keys = np.empty(st["refs"], dtype=np.uint32)
+        tris = np.empty(st["refs"], dtype=np.uint32)
+        beg = np.empty(st["cells"], dtype=np.uint32)
+        end = np.empty(st["cells"], dtype=np.uint32)
+        N.check(self._lib.cs_broadphase_dump(self._handle, geo, dims, keys.ctypes.data,
+                                             tris.ctypes.data, beg.ctypes.data, end.ctypes.data))
+        return {"origin": np.array(geo[0:3], dtype=np.float32), "inv_cell": np.float32(geo[3]),
+                "cell": np.float32(geo[4]), "dims": tuple(dims), "ref_keys": keys,
+                "ref_tris": tris, "cell_begin": beg, "cell_end": end}
 
     # -- runtime ------------------------------------------------------------------
     def set_external_accel(self, accel=None) -> None:

@@ -205,7 +205,34 @@ def kats():
     save("kats.npz", **out)
 
 
+def drift():
+    """BASELINE config 1 (64x64, two pinned corners, dt 0.004): the reference
+    float32 engine against the reference float64 solver, stepped in lockstep
+    from the same state -- max |dx| at steps 1/10/50/100.  This is the drift
+    any float32 implementation shows on this (chaotic) scene; the fast mode's
+    100-step gate is pinned to it instead of a hand-picked bound."""
+    mesh, params = corner_pinned(64, 0.004)
+    state = make_state(mesh)
+    eng = Engine(mesh, params=params)
+    checkpoints = (1, 10, 50, 100)
+    gaps, vgaps = [], []
+    out = {}
+    for f in range(1, max(checkpoints) + 1):
+        step(state, mesh, params)
+        eng.step()
+        if f in checkpoints:
+            gaps.append(np.abs(eng.read_positions().astype(np.float64) - state.positions).max())
+            vgaps.append(np.abs(eng.read_velocities().astype(np.float64) - state.velocities).max())
+            out[f"eng_pos_{f}"] = eng.read_positions()
+    ext = float((mesh.positions.max(axis=0) - mesh.positions.min(axis=0)).max())
+    out.update(checkpoints=np.array(checkpoints), eng_vs_sol_dx=np.array(gaps),
+               eng_vs_sol_dv=np.array(vgaps), extent=np.float64(ext))
+    print("C1 reference f32 engine vs f64 solver, max|dx|:", dict(zip(checkpoints, gaps)))
+    save("c1_drift.npz", **out)
+
+
 if __name__ == "__main__":
     topology()
     trajectories()
     kats()
+    drift()

@@ -113,3 +113,78 @@ def test_thread_count_does_not_change_bits():
     O.set_threads(1)
     np.testing.assert_array_equal(runs[0][1], runs[1][1])
     np.testing.assert_array_equal(runs[0][0], runs[1][0])
+
+
+def test_c1_drift_golden_reproduced_by_the_engine_oracle():
+    """tests/golden/c1_drift.npz holds the reference float32 engine's C1
+    positions at steps 1/10/50/100; the engine oracle reproduces them bit for
+    bit, and with the solver oracle the recorded drift."""
+    from paper_2507_11794_b200.scenes import baseline_scene
+
+    g = load_golden("c1_drift.npz")
+    sc = baseline_scene("C1")
+    eo = O.EngineOracle(sc.mesh, sc.params)
+    so = O.SolverOracle(sc.mesh, sc.params)
+    O.set_threads(O.max_threads())
+    done = 0
+    for cp, gap in zip(g["checkpoints"].tolist(), g["eng_vs_sol_dx"].tolist()):
+        for _ in range(cp - done):
+            eo.step()
+            so.step(normals=False)
+        done = cp
+        np.testing.assert_array_equal(eo.pos, g[f"eng_pos_{cp}"])
+        assert np.abs(eo.pos.astype(np.float64) - so.pos).max() == gap
+
+
+def _grid_loops(corners, cell_size=None):
+    """Plain-loop restatement of the cell assignment (small obstacles only)."""
+    origin, inv, _, dims = O.grid_geometry(corners, cell_size)
+    refs = []
+    for t, c in enumerate(np.asarray(corners, np.float32).reshape(-1, 3, 3)):
+        lo, hi = c.min(axis=0), c.max(axis=0)
+        a = O.grid_cell_of(lo, origin, inv, dims)
+        b = O.grid_cell_of(hi, origin, inv, dims)
+        for z in range(a[2], b[2] + 1):
+            for y in range(a[1], b[1] + 1):
+                for x in range(a[0], b[0] + 1):
+                    refs.append(((z * dims[1] + y) * dims[0] + x, t))
+    refs.sort(key=lambda r: r[0])  # stable: triangle order within a cell
+    return np.array(refs, dtype=np.int64).reshape(-1, 2)
+
+
+@pytest.mark.parametrize("sub,cell", [(1, None), (2, None), (2, 0.05), (3, 0.011)])
+def test_broadphase_restatement_is_a_conservative_prefilter(sub, cell):
+    """The grid restatement (oracle.broadphase_grid, the checker of the
+    device build) equals its plain-loop form, and as a prefilter it loses no
+    pair the reference's brute force would box-test: for random query boxes,
+    every triangle whose box overlaps the query is referenced by a cell of
+    the query's cell range (the contract of test_gpu_engine.py:267-307,
+    prefilter == brute force)."""
+    from paper_2507_11794_b200.mesh import generate_icosphere
+
+    ico = generate_icosphere(sub, radius=0.3, center=(0.1, -0.2, 0.3))
+    corners = np.asarray(ico.vertices)[np.asarray(ico.triangles)].astype(np.float32)
+    g = O.broadphase_grid(corners, cell)
+    loops = _grid_loops(corners, cell)
+    np.testing.assert_array_equal(g["ref_keys"], loops[:, 0])
+    np.testing.assert_array_equal(g["ref_tris"], loops[:, 1])
+    nz = g["cell_end"] > g["cell_begin"]
+    assert (g["cell_end"][nz] - g["cell_begin"][nz]).sum() == len(g["ref_keys"])
+    lo = corners.min(axis=1)
+    hi = corners.max(axis=1)
+    rng = np.random.default_rng(7)
+    for _ in range(200):
+        c = rng.uniform(-0.3, 0.5, size=3).astype(np.float32)
+        w = rng.uniform(0.0, 0.08, size=3).astype(np.float32)
+        ql, qh = c - w, c + w
+        brute = set(np.flatnonzero((lo <= qh).all(axis=1) & (hi >= ql).all(axis=1)).tolist())
+        a = O.grid_cell_of(ql, g["origin"], g["inv_cell"], g["dims"])
+        b = O.grid_cell_of(qh, g["origin"], g["inv_cell"], g["dims"])
+        dx, dy = g["dims"][0], g["dims"][1]
+        found = set()
+        for z in range(a[2], b[2] + 1):
+            for y in range(a[1], b[1] + 1):
+                for x in range(a[0], b[0] + 1):
+                    k = (z * dy + y) * dx + x
+                    found.update(g["ref_tris"][g["cell_begin"][k]:g["cell_end"][k]].tolist())
+        assert brute <= found
