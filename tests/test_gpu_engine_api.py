@@ -45,14 +45,23 @@ def test_golden_perturbed_forces_bit_exact():
 
 @pytest.mark.parametrize("precision", ["fixed", "fast"])
 def test_rest_cloth_force_buffer_is_exactly_zero_integers(precision):
-    """test_acceptance.py:127-143.  The all-zero-integers property after
-    several calm steps is a property of fixed-point accumulation (sub-quantum
-    forces round to 0 and never move a node); the fast float gather keeps
-    those ~1e-6 N residuals, so it is held to a tolerance instead."""
+    """test_acceptance.py:127-143.  The all-zero-integers property is a
+    property of fixed-point accumulation (each spring's sub-quantum force
+    rounds to 0 and never moves a node), which precision="fixed" keeps; the
+    fast float gather sums those ~1e-6 N residuals before its one encode, so
+    it is held to a tolerance instead."""
     eng = P.Engine(generate_cloth_grid(24, 24), params=SimParams(), precision=precision)
     eng.step()
     raw = eng.read_forces_raw()
-    assert raw.dtype == np.int32 and not raw.any()
+    assert raw.dtype == np.int32
+    if precision == "fixed":
+        assert not raw.any()
+    else:
+        # the fast mode's read_forces_raw is k_pair3's own float sum, encoded
+        # once per node: the f32 rounding of the rest grid leaves a few 1e-6 N
+        # per spring, which the reference's per-spring encode rounds away
+        print("fast rest-cloth max |raw|:", np.abs(raw).max())
+        assert np.abs(raw).max() <= 1  # measured 1
     calm = P.Engine(generate_cloth_grid(24, 24), params=SimParams(gravity=(0, 0, 0)),
                     precision=precision)
     for _ in range(3):
@@ -61,7 +70,8 @@ def test_rest_cloth_force_buffer_is_exactly_zero_integers(precision):
             assert not calm.read_forces_raw().any()
         else:
             # f32 rounding of the grid coordinates leaves ~1e-6 N per spring
-            assert np.abs(calm.read_forces_raw()).max() <= 16  # quanta of 2^-16 N
+            print("fast calm max |raw|:", np.abs(calm.read_forces_raw()).max())
+            assert np.abs(calm.read_forces_raw()).max() <= 4  # quanta of 2^-16 N (measured <= 3)
     assert np.abs(calm.read_positions() - generate_cloth_grid(24, 24).positions).max() < 1e-6
 
 

@@ -230,8 +230,12 @@ def test_c1_fast_drift_is_bounded_by_the_reference_engines_own():
 def test_fast_mode_golden_trajectories_within_tolerance(name):
     """Every golden scene (hanging, corner, drop, pull with ext accel, flags:
     substeps 2 + explicit Euler + raw response + margin 0.006) in the fast
-    mode: positions within 1e-3 of extent of the f64 solver at every
-    checkpoint, and within 1e-3 of the reference f32 engine."""
+    mode.  Over the whole run: within 1e-3 of extent of the f64 solver, or
+    within 2x the reference f32 engine's own distance from it where the
+    scene is chaotic (flags: the reference engine and solver end 3.6 apart
+    at frame 50 -- contact flips under the raw response).  From each
+    checkpoint's solver state (identical input): one fast frame within 1e-5
+    of extent of one solver frame (the per-step gate)."""
     g = load_golden(name)
     mesh, params, obs = mesh_from_golden(g), params_from_golden(g), obstacle_from_golden(g)
     eng = P.Engine(mesh, obstacle=obs, params=params, pair_budget=10**13)
@@ -244,6 +248,25 @@ def test_fast_mode_golden_trajectories_within_tolerance(name):
         done = cp
         got = eng.read_positions().astype(np.float64)
         d_sol = np.abs(got - g[f"sol_pos_{cp}"]).max()
-        d_eng = np.abs(got - g[f"eng_pos_{cp}"]).max()
-        print(f"{name} frame {cp}: vs solver {d_sol:.3e}, vs reference engine {d_eng:.3e}")
-        assert d_sol <= 1e-3 * ext and d_eng <= 1e-3 * ext, (cp, d_sol, d_eng)
+        d_ref = np.abs(g[f"eng_pos_{cp}"].astype(np.float64) - g[f"sol_pos_{cp}"]).max()
+        print(f"{name} frame {cp}: fast vs solver {d_sol:.3e}, reference engine vs solver "
+              f"{d_ref:.3e}")
+        assert d_sol <= max(1e-3 * ext, 2.0 * d_ref), (cp, d_sol, d_ref)
+    O.set_threads(O.max_threads())
+    for cp in g["checkpoints"].tolist():
+        pos = g[f"sol_pos_{cp}"].astype(np.float32)
+        vel = g[f"sol_vel_{cp}"].astype(np.float32)
+        one = P.Engine(mesh, obstacle=obs, params=params, pair_budget=10**13)
+        if "ext" in g:
+            one.set_external_accel(g["ext"])
+        one.write_positions(pos)
+        one.write_velocities(vel)
+        one.step()
+        so = O.SolverOracle(mesh, params, obs, external_accel=g.get("ext"))
+        so.pos[...] = pos.astype(np.float64)
+        so.vel[...] = vel.astype(np.float64)
+        so.step(normals=False)
+        dx = np.abs(one.read_positions().astype(np.float64) - so.pos).max()
+        dv = np.abs(one.read_velocities().astype(np.float64) - so.vel).max()
+        print(f"{name} one frame from frame {cp}: |dx| {dx:.3e}, |dv| {dv:.3e}")
+        assert dx <= 1e-5 * ext and dv <= 1e-5 * ext, (cp, dx, dv)
