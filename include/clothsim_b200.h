@@ -24,7 +24,9 @@
  *
  * All arguments are plain pointers and sizes.  Arrays passed to cs_create,
  * cs_write and cs_read are HOST arrays (row-major (N,3) float32 etc., the
- * reference's own buffer layouts); the library owns every device buffer.
+ * reference's own buffer layouts); cs_read_device / cs_write_device take
+ * DEVICE pointers (a PyTorch tensor's data_ptr()) in the same layouts and a
+ * stream.  The library owns the engine's own device buffers (SoA planes).
  * One handle = one CUDA stream; calls on a handle are not thread-safe, as in
  * the reference.  Every function returns 0 on success or a
  * negative CS_E* code; cs_last_error() returns the message.
@@ -275,6 +277,27 @@ int cs_mem_info(int64_t *free_bytes, int64_t *total_bytes);
    u64.  Bit-identical pixels to the reference (float64, numpy's operation
    order, strict-greater z test with earlier-triangle ties). */
 int cs_snapshot_bounds(const double *verts, int64_t n, double out[6], void *stream);
+/* ---- device-pointer boundary (PyTorch tensors: tensor.data_ptr(), the
+   reference's readbacks gpu/engine.py:362-378 and writes through
+   Engine.buffers / set_external_accel engine.py:297-302, without a host
+   copy) ----
+   cs_read_device transposes buffer `id` into DEVICE memory `dev_dst` in the
+   reference's (N,3) row-major layout (N for CS_BUF_COUNTS): f32 for
+   POSITIONS / VELOCITIES / PREV_POSITIONS / NORMALS / NORMALS_LAGGED (a
+   float64 engine converts), f64 for POSITIONS64 / VELOCITIES64, i32 for
+   ACCUMULATOR / COUNTS.  cs_write_device is the inverse for POSITIONS /
+   VELOCITIES (f32), POSITIONS64 / VELOCITIES64 (f64, float64 engines) and
+   EXT_ACCEL (f32).  Both are enqueued on `stream` (NULL = the engine's),
+   ordered after the engine's earlier work and before its later work by
+   events; neither synchronises the host nor touches host memory.
+   cs_set_stream moves the engine to another stream for every later call
+   (work already enqueued on the old stream stays ordered before it). */
+int cs_read_device(cs_engine *h, int32_t buffer_id, void *dev_dst, void *stream);
+int cs_write_device(cs_engine *h, int32_t buffer_id, const void *dev_src, void *stream);
+int cs_set_stream(cs_engine *h, void *stream);
+/* The CUDA device ordinal the engine was created on (its buffers live there;
+   device pointers passed to it must too). */
+int cs_device(cs_engine *h, int32_t *device);
 /* The engine's current positions as DEVICE float64 (N, 3), enqueued on the
    engine's stream (cs_stream): the snapshot's cloth vertices without a
    host round trip (bench.py:186 reads them back in the reference). */

@@ -131,6 +131,10 @@ SIGNATURES = {
     "cs_broadphase_dump": (_I32, [_P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(_I32), _P,
                                   _P, _P, _P]),
     "cs_positions_device": (_I32, [_P, _P]),
+    "cs_read_device": (_I32, [_P, _I32, _P, _P]),
+    "cs_write_device": (_I32, [_P, _I32, _P, _P]),
+    "cs_set_stream": (_I32, [_P, _P]),
+    "cs_device": (_I32, [_P, ctypes.POINTER(_I32)]),
     "cs_snapshot_bounds": (_I32, [_P, _I64, ctypes.POINTER(ctypes.c_double), _P]),
     "cs_snapshot_render": (_I32, [_P, _P, _I64, _I64, ctypes.POINTER(ctypes.c_double),
                                   ctypes.POINTER(_I32), _I32, _I32, _P, _P, _P]),

@@ -54,6 +54,7 @@ struct cs_engine {
     cudaStream_t st = nullptr;
     bool own_stream = false;
     int num_sms = 148;
+    int device = 0;  // the CUDA device the engine's buffers live on
     int substeps = 1;
     bool average = true;
 
@@ -119,6 +120,9 @@ struct cs_engine {
     // cs_record: copy stream, per-parity events and device staging
     cudaStream_t copy_st = nullptr;
     cudaEvent_t ev_frame[2] = {nullptr, nullptr}, ev_moved[2] = {nullptr, nullptr};
+    // cross-stream ordering of device-pointer transfers (cs_read_device /
+    // cs_write_device / cs_set_stream)
+    cudaEvent_t ev_join = nullptr;
     float *rec_stage[2] = {nullptr, nullptr};
     int64_t frames = 0;
     // row band (cs_set_halo_peers): neighbours' buffers + per-pass handshake
@@ -200,6 +204,24 @@ __global__ void k_planes_to_aos64(int64_t N, int64_t nx, int64_t pitch, int64_t 
     if (n >= N) return;
     const int64_t g = (n / nx) * pitch + (n % nx);
     for (int c = 0; c < 3; ++c) aos[n * 3 + c] = (double)planes[c * plane + g];
+}
+// planes (pitch layout) <-> (N, comps) AoS with a type conversion: the
+// device-pointer transfers (a float64 engine's f32 views, f32 -> f64 writes)
+template <typename Ti, typename To>
+__global__ void k_planes_to_aos_cvt(int64_t N, int64_t nx, int64_t pitch, int64_t plane, int comps,
+                                    const Ti *__restrict__ planes, To *__restrict__ aos) {
+    const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    const int64_t g = (n / nx) * pitch + (n % nx);
+    for (int c = 0; c < comps; ++c) aos[n * comps + c] = (To)planes[c * plane + g];
+}
+template <typename Ti, typename To>
+__global__ void k_aos_to_planes_cvt(int64_t N, int64_t nx, int64_t pitch, int64_t plane, int comps,
+                                    const Ti *__restrict__ aos, To *__restrict__ planes) {
+    const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    const int64_t g = (n / nx) * pitch + (n % nx);
+    for (int c = 0; c < comps; ++c) planes[c * plane + g] = (To)aos[n * comps + c];
 }
 __global__ void k_f64_to_f32(int64_t n, const double *a, float *b) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -569,6 +591,7 @@ static int build(cs_engine *h, const cs_desc *d) {
 
     int dev = 0;
     CK(cudaGetDevice(&dev));
+    h->device = dev;
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (d->stream) {
         h->st = (cudaStream_t)d->stream;
@@ -817,6 +840,7 @@ extern "C" int cs_destroy(cs_engine *h) {
     }
     if (h->clog) cudaFree(h->clog);
     if (h->clog_n) cudaFree(h->clog_n);
+    if (h->ev_join) cudaEventDestroy(h->ev_join);
     for (int i = 0; i < 2; ++i) {
         if (h->ev_frame[i]) cudaEventDestroy(h->ev_frame[i]);
         if (h->ev_moved[i]) cudaEventDestroy(h->ev_moved[i]);
@@ -1185,6 +1209,123 @@ extern "C" int cs_write(cs_engine *h, int32_t id, const void *src) {
         default:
             return fail(CS_E_INVALID, "unknown or read-only buffer id");
     }
+}
+
+// ---- device-pointer transfers (PyTorch tensors: tensor.data_ptr()) ------------------
+// `to` waits for everything enqueued on `from` so far
+static int join(cs_engine *h, cudaStream_t from, cudaStream_t to) {
+    if (from == to) return 0;
+    if (!h->ev_join) CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+    CK(cudaEventRecord(h->ev_join, from));
+    CK(cudaStreamWaitEvent(to, h->ev_join, 0));
+    return 0;
+}
+
+extern "C" int cs_device(cs_engine *h, int32_t *device) {
+    if (!h || !device) return fail(CS_E_INVALID, "null argument");
+    *device = h->device;
+    return 0;
+}
+
+extern "C" int cs_set_stream(cs_engine *h, void *stream) {
+    if (!h) return fail(CS_E_INVALID, "null engine");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!s) return fail(CS_E_INVALID, "pass a real CUDA stream (the legacy default stream is not one)");
+    if (h->banded) return fail(CS_E_INVALID, "a linked row band keeps its stream");
+    if (s == h->st) return 0;
+    if (int r = join(h, h->st, s)) return r;  // the new stream continues after the old one's work
+    if (h->copy_st) CK(cudaStreamSynchronize(h->copy_st));
+    if (h->own_stream) {
+        CK(cudaStreamSynchronize(h->st));
+        CK(cudaStreamDestroy(h->st));
+        h->own_stream = false;
+    }
+    h->st = s;  // captured graphs are stream-independent: cudaGraphLaunch takes the stream
+    return 0;
+}
+
+extern "C" int cs_read_device(cs_engine *h, int32_t id, void *dst, void *stream) {
+    if (!h || !dst) return fail(CS_E_INVALID, "null argument");
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->st;
+    const int64_t P = h->plane, nxx = h->grid ? h->nx : h->N;
+    const void *base = nullptr;
+    int comps = 3;
+    bool wide = h->fp64, i32 = false, want64 = false;
+    switch (id) {
+        case CS_BUF_POSITIONS: case CS_BUF_POSITIONS64: base = h->state[h->cur]; break;
+        case CS_BUF_VELOCITIES: case CS_BUF_VELOCITIES64:
+            base = (const char *)h->state[h->cur] + 3 * P * h->esz;
+            break;
+        case CS_BUF_PREV_POSITIONS: base = h->state[1 - h->cur]; break;
+        case CS_BUF_NORMALS: flush_normals(h); base = h->normals; break;
+        case CS_BUF_NORMALS_LAGGED: base = h->normals; break;
+        case CS_BUF_ACCUMULATOR: base = h->acc; wide = false; i32 = true; break;
+        case CS_BUF_COUNTS: base = h->count; wide = false; i32 = true; comps = 1; break;
+        default: return fail(CS_E_INVALID, "buffer id not readable into device memory");
+    }
+    if (id == CS_BUF_POSITIONS64 || id == CS_BUF_VELOCITIES64) {
+        if (!h->fp64) return fail(CS_E_INVALID, "float64 buffers need a CS_FLAG_FP64 engine");
+        want64 = true;
+    }
+    if (h->banded)
+        if (int r = halo_wait(h)) return r;  // halo rows of the current state landed
+    if (int r = join(h, h->st, s)) return r;
+    const unsigned g = nb(h->N);
+    if (i32)
+        k_planes_to_aos_cvt<int32_t, int32_t><<<g, 256, 0, s>>>(h->N, nxx, h->pitch, P, comps,
+                                                                (const int32_t *)base, (int32_t *)dst);
+    else if (wide && want64)
+        k_planes_to_aos_cvt<double, double><<<g, 256, 0, s>>>(h->N, nxx, h->pitch, P, 3,
+                                                              (const double *)base, (double *)dst);
+    else if (wide)
+        k_planes_to_aos_cvt<double, float><<<g, 256, 0, s>>>(h->N, nxx, h->pitch, P, 3,
+                                                             (const double *)base, (float *)dst);
+    else
+        k_planes_to_aos_cvt<float, float><<<g, 256, 0, s>>>(h->N, nxx, h->pitch, P, 3,
+                                                            (const float *)base, (float *)dst);
+    CK(cudaGetLastError());
+    return join(h, s, h->st);  // later frames may not overwrite the state under the read
+}
+
+extern "C" int cs_write_device(cs_engine *h, int32_t id, const void *src, void *stream) {
+    if (!h || !src) return fail(CS_E_INVALID, "null argument");
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->st;
+    const int64_t P = h->plane, nxx = h->grid ? h->nx : h->N;
+    void *base = nullptr;
+    bool src64 = false;
+    switch (id) {
+        case CS_BUF_POSITIONS: base = h->state[h->cur]; break;
+        case CS_BUF_VELOCITIES: base = (char *)h->state[h->cur] + 3 * P * h->esz; break;
+        case CS_BUF_POSITIONS64: src64 = true; base = h->state[h->cur]; break;
+        case CS_BUF_VELOCITIES64: src64 = true; base = (char *)h->state[h->cur] + 3 * P * h->esz; break;
+        case CS_BUF_EXT_ACCEL:
+            if (!h->ext) {
+                CK(cudaMalloc(&h->ext, 3 * P * h->esz));
+                CK(cudaMemsetAsync(h->ext, 0, 3 * P * h->esz, h->st));
+                drop_graphs(h);  // kernels now read the ext planes
+            }
+            h->has_ext = true;
+            base = h->ext;
+            break;
+        default: return fail(CS_E_INVALID, "buffer id not writable from device memory");
+    }
+    if (src64 && !h->fp64) return fail(CS_E_INVALID, "float64 buffers need a CS_FLAG_FP64 engine");
+    if (id == CS_BUF_POSITIONS || id == CS_BUF_VELOCITIES || src64) flush_normals(h);
+    if (h->banded)
+        if (int r = halo_wait(h)) return r;
+    if (int r = join(h, h->st, s)) return r;
+    const unsigned g = nb(h->N);
+    if (src64)
+        k_aos_to_planes_cvt<double, double><<<g, 256, 0, s>>>(h->N, nxx, h->pitch, P, 3,
+                                                              (const double *)src, (double *)base);
+    else if (h->fp64)
+        k_aos_to_planes_cvt<float, double><<<g, 256, 0, s>>>(h->N, nxx, h->pitch, P, 3,
+                                                             (const float *)src, (double *)base);
+    else
+        k_aos_to_planes_cvt<float, float><<<g, 256, 0, s>>>(h->N, nxx, h->pitch, P, 3,
+                                                            (const float *)src, (float *)base);
+    CK(cudaGetLastError());
+    return join(h, s, h->st);  // the next frame reads the new state
 }
 
 extern "C" int cs_inject_response(cs_engine *h, int64_t node, const int32_t raw[3], int32_t count) {

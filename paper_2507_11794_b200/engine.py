@@ -227,6 +227,15 @@ def _p(a):
     return None if a is None else a.ctypes.data
 
 
+def _is_cuda_tensor(x) -> bool:
+    """A torch CUDA tensor (duck-typed: torch is imported only by callers)."""
+    return getattr(x, "is_cuda", False) is True and hasattr(x, "data_ptr")
+
+
+_TORCH_DTYPE_NAMES = {np.dtype(np.float32): "torch.float32", np.dtype(np.float64): "torch.float64",
+                      np.dtype(np.int32): "torch.int32"}
+
+
 def pinned_empty(shape, dtype=np.float32) -> np.ndarray:
     """Page-locked host array (through torch's pinned allocator when torch is
     importable, else an ordinary numpy array)."""
@@ -454,6 +463,9 @@ class Engine:
         if accel is None:
             N.check(self._lib.cs_write(self._handle, N.BUF_EXT_ACCEL, None))
             return
+        if _is_cuda_tensor(accel):
+            self._write(N.BUF_EXT_ACCEL, accel)
+            return
         a = np.ascontiguousarray(np.broadcast_to(np.asarray(accel, dtype=_F32),
                                                  (self.num_nodes, 3)))
         N.check(self._lib.cs_write(self._handle, N.BUF_EXT_ACCEL, a.ctypes.data))
@@ -564,15 +576,57 @@ class Engine:
                 "hit_counter": s.hit_counter}
 
     # -- transfers ------------------------------------------------------------------
+    # Every read_* / write_* accepts either host arrays (the reference's numpy
+    # readbacks, engine.py:362-378) or torch CUDA tensors: those move device
+    # to device (cs_read_device / cs_write_device), enqueued on the tensor's
+    # device's current torch stream and event-ordered against the engine's
+    # own stream -- no host copy, no synchronisation.
+    @property
+    def cuda_device(self) -> int:
+        d = ctypes.c_int32()
+        N.check(self._lib.cs_device(self._handle, ctypes.byref(d)))
+        return d.value
+
+    def _check_tensor(self, t, dtype, shape):
+        if str(t.dtype) != _TORCH_DTYPE_NAMES[np.dtype(dtype)] or tuple(t.shape) != shape \
+                or not t.is_contiguous():
+            raise ValueError(f"tensor must be a contiguous {_TORCH_DTYPE_NAMES[np.dtype(dtype)]} "
+                             f"CUDA tensor of shape {shape}")
+        if t.device.index != self.cuda_device:
+            raise ValueError(f"tensor is on cuda:{t.device.index}, the engine on "
+                             f"cuda:{self.cuda_device}")
+
+    @staticmethod
+    def _torch_stream(t) -> int:
+        import torch
+
+        return torch.cuda.current_stream(t.device).cuda_stream
+
     def _read(self, buf, dtype, comps, out=None):
         shape = (self.num_nodes, comps) if comps > 1 else (self.num_nodes,)
+        if out is not None and _is_cuda_tensor(out):
+            self._check_tensor(out, dtype, shape)
+            N.check(self._lib.cs_read_device(self._handle, buf, out.data_ptr(),
+                                             self._torch_stream(out)))
+            return out
         if out is None:
             out = np.empty(shape, dtype=dtype)
         N.check(self._lib.cs_read(self._handle, buf, out.ctypes.data))
         return out
 
-    def _write(self, buf, arr):
+    def _write(self, buf, arr, dtype=np.float32):
+        if _is_cuda_tensor(arr):
+            self._check_tensor(arr, dtype, (self.num_nodes, 3))
+            N.check(self._lib.cs_write_device(self._handle, buf, arr.data_ptr(),
+                                              self._torch_stream(arr)))
+            return
         N.check(self._lib.cs_write(self._handle, buf, np.ascontiguousarray(arr).ctypes.data))
+
+    def set_stream(self, stream) -> None:
+        """Launch every later frame / transfer on `stream` (a torch.cuda.Stream
+        or a cudaStream_t handle); work already enqueued stays ordered first."""
+        handle = int(getattr(stream, "cuda_stream", stream))
+        N.check(self._lib.cs_set_stream(self._handle, handle))
 
     def read_positions(self, out=None) -> np.ndarray:
         return self._read(N.BUF_POSITIONS, _F32, 3, out)
@@ -589,8 +643,8 @@ class Engine:
         stand-alone recompute read_normals() does for the current state."""
         return self._read(N.BUF_NORMALS_LAGGED, _F32, 3, out)
 
-    def read_previous_positions(self) -> np.ndarray:
-        return self._read(N.BUF_PREV_POSITIONS, _F32, 3)
+    def read_previous_positions(self, out=None) -> np.ndarray:
+        return self._read(N.BUF_PREV_POSITIONS, _F32, 3, out)
 
     def read_forces_raw(self) -> np.ndarray:
         """Spring-only i32 fixed-point forces of the last spring pass
@@ -598,29 +652,29 @@ class Engine:
         reference engine's exact arithmetic."""
         return self._read(N.BUF_FORCES_RAW, np.int32, 3)
 
-    def read_accumulator_raw(self) -> np.ndarray:
-        return self._read(N.BUF_ACCUMULATOR, np.int32, 3)
+    def read_accumulator_raw(self, out=None) -> np.ndarray:
+        return self._read(N.BUF_ACCUMULATOR, np.int32, 3, out)
 
-    def read_counts(self) -> np.ndarray:
-        return self._read(N.BUF_COUNTS, np.int32, 1)
+    def read_counts(self, out=None) -> np.ndarray:
+        return self._read(N.BUF_COUNTS, np.int32, 1, out)
 
-    def read_positions64(self) -> np.ndarray:
-        return self._read(N.BUF_POSITIONS64, np.float64, 3)
+    def read_positions64(self, out=None) -> np.ndarray:
+        return self._read(N.BUF_POSITIONS64, np.float64, 3, out)
 
-    def read_velocities64(self) -> np.ndarray:
-        return self._read(N.BUF_VELOCITIES64, np.float64, 3)
+    def read_velocities64(self, out=None) -> np.ndarray:
+        return self._read(N.BUF_VELOCITIES64, np.float64, 3, out)
 
     def write_positions(self, arr) -> None:
-        self._write(N.BUF_POSITIONS, np.asarray(arr, dtype=_F32))
+        self._write(N.BUF_POSITIONS, arr if _is_cuda_tensor(arr) else np.asarray(arr, dtype=_F32))
 
     def write_velocities(self, arr) -> None:
-        self._write(N.BUF_VELOCITIES, np.asarray(arr, dtype=_F32))
+        self._write(N.BUF_VELOCITIES, arr if _is_cuda_tensor(arr) else np.asarray(arr, dtype=_F32))
 
     def write_state64(self, pos=None, vel=None) -> None:
-        if pos is not None:
-            self._write(N.BUF_POSITIONS64, np.asarray(pos, dtype=np.float64))
-        if vel is not None:
-            self._write(N.BUF_VELOCITIES64, np.asarray(vel, dtype=np.float64))
+        for buf, a in ((N.BUF_POSITIONS64, pos), (N.BUF_VELOCITIES64, vel)):
+            if a is not None:
+                self._write(buf, a if _is_cuda_tensor(a) else np.asarray(a, dtype=np.float64),
+                            dtype=np.float64)
 
     def render_snapshot(self, size=(320, 240), axis: str = "y", obstacle: bool = True) -> np.ndarray:
         """uint8 (H, W, 3) pixels of the current frame's snapshot (io.py:225-287),
