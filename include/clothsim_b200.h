@@ -289,7 +289,8 @@ int cs_snapshot_bounds(const double *verts, int64_t n, double out[6], void *stre
    VELOCITIES (f32), POSITIONS64 / VELOCITIES64 (f64, float64 engines) and
    EXT_ACCEL (f32).  Both are enqueued on `stream` (NULL = the engine's),
    ordered after the engine's earlier work and before its later work by
-   events; neither synchronises the host nor touches host memory.
+   events; neither synchronises the host nor touches host memory (the
+   legacy default stream is cudaStreamLegacy, (void *)1).
    cs_set_stream moves the engine to another stream for every later call
    (work already enqueued on the old stream stays ordered before it). */
 int cs_read_device(cs_engine *h, int32_t buffer_id, void *dev_dst, void *stream);

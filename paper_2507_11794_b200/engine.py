@@ -598,9 +598,12 @@ class Engine:
 
     @staticmethod
     def _torch_stream(t) -> int:
+        """The tensor's device's current torch stream as a cudaStream_t; torch's
+        default stream is the legacy default stream, handle 0, which the C ABI
+        reads as "the engine's stream" -- pass cudaStreamLegacy (1) instead."""
         import torch
 
-        return torch.cuda.current_stream(t.device).cuda_stream
+        return torch.cuda.current_stream(t.device).cuda_stream or 1
 
     def _read(self, buf, dtype, comps, out=None):
         shape = (self.num_nodes, comps) if comps > 1 else (self.num_nodes,)

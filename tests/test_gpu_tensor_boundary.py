@@ -106,7 +106,7 @@ def test_float64_and_collision_buffers_through_tensors():
     from paper_2507_11794_b200 import _native as N
 
     f = P.Engine(sc.mesh, sc.obstacle, sc.params, pair_budget=10**12)
-    f.step_frames(80)
+    f.step_frames(150)
     N.check(f._lib.cs_run_pass(f._handle, N.PASS_FORCE_INTEGRATE))
     N.check(f._lib.cs_run_pass(f._handle, N.PASS_DETECT))
     acc = torch.empty((sc.mesh.num_nodes, 3), dtype=torch.int32, device="cuda")
