@@ -24,7 +24,10 @@ vertex normals.  Synthetic inputs (the reference's own scene builder).
 * cpu_baseline the CPU oracle (restatement of the reference float64 solver,
                oracle/) on this host's cores, bounded sample of the workload.
 * collision    config 3 (316x316 vs the 99,904-triangle sphere) steps/s after
-               a 200-frame drape.
+               a 200-frame drape, with its own cpu_baseline: the reference
+               solver's brute-force detect_all restated in oracle/, measured
+               pairs/s on a bounded slice, frame time extrapolated (labelled).
+* collision_c4 the same for config 4 (64x64 vs the same sphere).
 
 N>1 (torchrun): config 5 (4096^2) row-band partitioned, 2-row halos
 stored into the neighbours by the step kernel itself (peer memory through
@@ -364,7 +367,8 @@ def main():
         "e2e_device": e2e_device,
     }
     if not args.no_collision and config_name == "C2":
-        line["collision"] = collision_bench(P, torch, args)
+        line["collision"] = collision_bench(P, torch, args, "C3", cpu=not args.no_cpu_baseline)
+        line["collision_c4"] = collision_bench(P, torch, args, "C4", cpu=not args.no_cpu_baseline)
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(scene)
     print(json.dumps(line))
@@ -474,8 +478,89 @@ def band_projection(P, torch, stream, scene_params, k, frame_ms):
                     "(rows incl. 2+2 halo rows); the per-frame seam exchange is not included"}
 
 
-def collision_bench(P, torch, args):
-    scene = P.baseline_scene("C3")
+def collision_cpu_baseline(scene, positions, seconds=20.0):
+    """The reference CPU path of a collision frame: solver.step with
+    detect_all's brute force (collision.py:243-315; E*T + 3*T*C float64
+    segment-triangle tests per frame, no broad phase), restated in oracle/
+    (OpenMP over all host cores).  A whole C3 frame is 9.0e10 tests (hours
+    of CPU), so this is a bounded sample, extrapolated and labelled as such:
+    pass A on a strided slice of the cloth edges against every obstacle
+    triangle, pass B on a strided slice of the obstacle's triangles (their 3
+    edges) against every cloth triangle, both at the draped state the GPU
+    measured, plus measured spring + integrate steps of the same cloth; the
+    frame time is the step time plus each pass's pair count over its
+    measured pairs/s."""
+    import ctypes
+
+    from oracle import oracle as O
+    from paper_2507_11794_b200.mesh import grid_unique_edges
+
+    L = O.lib()
+    threads = O.max_threads()
+    O.set_threads(threads)
+    mesh, obs, prm = scene.mesh, scene.obstacle, scene.params
+    n = mesh.num_nodes
+    pos = np.ascontiguousarray(positions, dtype=np.float64)
+    edges = np.ascontiguousarray(grid_unique_edges(mesh.nx, mesh.ny), dtype=np.int32)
+    tris = np.ascontiguousarray(mesh.triangles, dtype=np.int32)
+    overt = np.ascontiguousarray(obs.vertices, dtype=np.float64)
+    otris = np.ascontiguousarray(obs.triangles, dtype=np.int32)
+    onorm = np.ascontiguousarray(obs.face_normals, dtype=np.float64)
+    acc = np.zeros((n, 3))
+    cnt = np.zeros(n, dtype=np.int64)
+    E, C, T = len(edges), len(tris), len(otris)
+    p = lambda a: a.ctypes.data  # noqa: E731
+
+    def pass_a(k):  # k cloth edges (strided) vs every obstacle triangle
+        e = np.ascontiguousarray(edges[:: max(1, E // k)][:k])
+        t0 = time.perf_counter()
+        L.or_sol_detect(n, p(pos), len(e), p(e), 0, p(tris), T, p(overt), p(otris), p(onorm),
+                        float(prm.epsilon_mt), float(prm.response_margin), p(acc), p(cnt))
+        return len(e) * T, time.perf_counter() - t0
+
+    def pass_b(k):  # the 3 edges of k obstacle triangles (strided) vs every cloth triangle
+        sl = otris[:: max(1, T // k)][:k]
+        o = np.ascontiguousarray(sl)
+        on = np.ascontiguousarray(onorm[:: max(1, T // k)][:k])
+        t0 = time.perf_counter()
+        L.or_sol_detect(n, p(pos), 0, p(edges), C, p(tris), len(o), p(overt), p(o), p(on),
+                        float(prm.epsilon_mt), float(prm.response_margin), p(acc), p(cnt))
+        return 3 * len(o) * C, time.perf_counter() - t0
+
+    budget = seconds / 3.0
+    rates = {}
+    for name, fn, units in (("pass_a", pass_a, E), ("pass_b", pass_b, T)):
+        pairs, dt = fn(max(1, min(units, 64)))  # calibration slice
+        rate = pairs / max(dt, 1e-9)
+        per_unit = pairs / max(1, min(units, 64))
+        k = int(max(1, min(units, budget * rate / per_unit)))
+        pairs, dt = fn(k)
+        rates[name] = {"pairs": pairs, "seconds": dt, "pairs_per_s": pairs / dt,
+                       "slice": f"{k} of {units} {'cloth edges' if name == 'pass_a' else 'obstacle triangles'}"}
+    so = O.SolverOracle(mesh, prm)  # spring + integrate (+ normals) of the same cloth
+    so.pos[...] = pos
+    so.step()
+    t0 = time.perf_counter()
+    k = 0
+    while k < 50 and time.perf_counter() - t0 < budget:
+        so.step()
+        k += 1
+    t_step = (time.perf_counter() - t0) / k
+    t_a = E * T / rates["pass_a"]["pairs_per_s"]
+    t_b = 3 * T * C / rates["pass_b"]["pairs_per_s"]
+    frame = t_step + t_a + t_b
+    return {"value": 1.0 / frame, "unit": "steps/s", "cores": threads, "kind": "port",
+            "extrapolated": True,
+            "sample": (f"oracle/ float64 solver.step restatement, {threads} threads: pass A "
+                       f"{rates['pass_a']['slice']}, pass B {rates['pass_b']['slice']} (measured "
+                       f"pairs/s at the draped GPU state), {k} spring+integrate steps; frame = "
+                       f"step + (E*T)/rate_A + (3*T*C)/rate_B, E={E} T={T} C={C}"),
+            "seconds_per_frame": frame, "step_seconds": t_step, "detect_seconds": t_a + t_b,
+            "passes": rates}
+
+
+def collision_bench(P, torch, args, config="C3", cpu=True):
+    scene = P.baseline_scene(config)
     stream = torch.cuda.Stream()  # a real stream: the legacy default (0) would mean "own stream"
     torch.cuda.set_stream(stream)
     eng = P.Engine(scene.mesh, scene.obstacle, scene.params, pair_budget=10**13,
@@ -501,7 +586,7 @@ def collision_bench(P, torch, args):
     frame_bytes = 60 * n_nodes + 48 * n_tris + 40 * int(touched)
     peak, _ = _peaks()
     achieved = frame_bytes / (ms * 1e-3) / 1e9
-    return {"workload": "C3: " + P.scenes.BASELINE_CONFIGS["C3"], "steps_per_s": 1000.0 / ms,
+    out = {"workload": f"{config}: " + P.scenes.BASELINE_CONFIGS[config], "steps_per_s": 1000.0 / ms,
             "ms_per_step": ms, "node_updates_per_s": 1000.0 / ms * scene.mesh.num_nodes,
             "roofline": {"bound": "latency (dependent grid lookups per query; SURVEY 8(d))",
                          "bytes_per_frame": frame_bytes, "achieved": achieved, "peak": peak,
@@ -509,6 +594,10 @@ def collision_bench(P, torch, args):
             "contacts_per_step": (st["hit_counter"] - hits_before) / k,
             "finite": bool(np.isfinite(pos).all()), "kernels_per_frame": eng.kernels_per_frame,
             "broadphase": eng.broadphase_stats()}
+    eng.close()
+    if cpu:
+        out["cpu_baseline"] = collision_cpu_baseline(scene, pos)
+    return out
 
 
 if __name__ == "__main__":

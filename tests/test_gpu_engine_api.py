@@ -251,3 +251,23 @@ def test_lagged_normals_are_the_previous_frames_normals(scene):
     split.step_frames(39)
     np.testing.assert_array_equal(fused.read_normals_lagged(), split.read_normals())
     np.testing.assert_array_equal(fused.read_previous_positions(), split.read_positions())
+
+
+def test_fp64_state_view_assignment_keeps_every_other_node_bit_exact():
+    """eng.buffers.vel[0] = ... on a float64 engine goes through the f64
+    buffers: the assigned node gets the value, every other node keeps its
+    float64 state bit for bit (no f32 round trip)."""
+    sc = P.build_scene(P.ScenarioConfig("hanging", (8, 8), dt=0.004))
+    eng = P.Engine(sc.mesh, params=sc.params, precision="fp64")
+    eng.step_frames(5)
+    p0, v0 = eng.read_positions64(), eng.read_velocities64()
+    assert eng.buffers.vel.dtype == np.float64
+    eng.buffers.vel[3] = (0.0, 0.0, 2.0)
+    eng.buffers.pos[5] = (0.1, 0.2, 0.30000000000000004)
+    p1, v1 = eng.read_positions64(), eng.read_velocities64()
+    keep = np.ones(len(p0), dtype=bool)
+    keep[[3, 5]] = False
+    np.testing.assert_array_equal(v1[np.arange(len(v0)) != 3], v0[np.arange(len(v0)) != 3])
+    np.testing.assert_array_equal(p1[np.arange(len(p0)) != 5], p0[np.arange(len(p0)) != 5])
+    np.testing.assert_array_equal(v1[3], (0.0, 0.0, 2.0))
+    np.testing.assert_array_equal(p1[5], (0.1, 0.2, 0.30000000000000004))
