@@ -76,6 +76,10 @@ extern "C" {
                                        warp, flattened over cells/candidates) */
 #define CS_FLAG_WARP_NARROW 2048u   /* collision narrow phase: one warp per
                                        query */
+#define CS_FLAG_NO_PERSIST 4096u  /* never use the persistent multi-pass kernel
+                                       (multi-frame steps and row bands then
+                                       launch one kernel per frame, bands with
+                                       the stream-memop seam handshake) */
 #define CS_FLAG_PAIRED 128u         /* fast mode: the paired-column f32x2
                                        warp-strip kernel (cs_pair3.cu, the
                                        production path; Engine kernel="pair")
@@ -176,7 +180,11 @@ typedef struct cs_stats {
 
 int cs_create(const cs_desc *desc, cs_engine **out);
 int cs_destroy(cs_engine *h);
-/* Advance `frames` whole frames (asynchronous on the engine's stream). */
+/* Advance `frames` whole frames (asynchronous on the engine's stream).  A
+   fast, collision-free grid engine with fused normals runs frames >= 2 (and
+   a linked row band every call) as ONE persistent launch whose chunks are
+   ordered by per-chunk flags instead of kernel boundaries; otherwise each
+   frame replays the frame's CUDA graph. */
 int cs_step(cs_engine *h, int32_t frames);
 int cs_run_pass(cs_engine *h, int32_t pass_id);
 /* Advance `frames` frames, streaming every frame's positions ((N,3) f32) into

@@ -256,7 +256,7 @@ class Engine:
                  pair_budget: int = DEFAULT_PAIR_BUDGET, *, precision: str = "fast",
                  graph: bool = True, stream=None, cell_size: float | None = None,
                  force_csr: bool = False, kernel: str = "pair", narrow: str = "batch",
-                 normals: str = "auto"):
+                 normals: str = "auto", persist: bool = True):
         if precision not in PRECISIONS:
             raise ValueError(f"precision must be one of {PRECISIONS}")
         self.mesh = mesh
@@ -352,6 +352,8 @@ class Engine:
             flags |= N.FLAG_WARP_NARROW
         if kernel == "pair":
             flags |= N.FLAG_PAIRED
+        if not persist:
+            flags |= N.FLAG_NO_PERSIST
         d.flags = flags
         if stencil is not None:
             d.nx, d.ny = stencil[0], stencil[1]
