@@ -76,10 +76,10 @@ extern "C" {
                                        warp, flattened over cells/candidates) */
 #define CS_FLAG_WARP_NARROW 2048u   /* collision narrow phase: one warp per
                                        query */
-#define CS_FLAG_NO_PERSIST 4096u  /* never use the persistent multi-pass kernel
-                                       (multi-frame steps and row bands then
-                                       launch one kernel per frame, bands with
-                                       the stream-memop seam handshake) */
+#define CS_FLAG_MEMOP_SEAM 4096u  /* row bands: the stream-memop seam handshake
+                                       (cuStreamWaitValue32 / WriteValue32
+                                       around each pass, no graph) even where
+                                       the fast kernel could do it in-kernel */
 #define CS_FLAG_PAIRED 128u         /* fast mode: the paired-column f32x2
                                        warp-strip kernel (cs_pair3.cu, the
                                        production path; Engine kernel="pair")
@@ -180,11 +180,7 @@ typedef struct cs_stats {
 
 int cs_create(const cs_desc *desc, cs_engine **out);
 int cs_destroy(cs_engine *h);
-/* Advance `frames` whole frames (asynchronous on the engine's stream).  A
-   fast, collision-free grid engine with fused normals runs frames >= 2 (and
-   a linked row band every call) as ONE persistent launch whose chunks are
-   ordered by per-chunk flags instead of kernel boundaries; otherwise each
-   frame replays the frame's CUDA graph. */
+/* Advance `frames` whole frames (asynchronous on the engine's stream). */
 int cs_step(cs_engine *h, int32_t frames);
 int cs_run_pass(cs_engine *h, int32_t pass_id);
 /* Advance `frames` frames, streaming every frame's positions ((N,3) f32) into
@@ -227,9 +223,15 @@ int cs_state_plane(cs_engine *h, int32_t which, void **dev_ptr, int64_t *pitch);
    my rows [src_row0, src_row0+rows) straight into its rows
    [dst_row0, dst_row0+rows) -- the halo exchange happens inside the step, as
    peer stores over NVLink -- then signals `remote_flag` (the neighbour's flag
-   word 0 if I am its upper neighbour, 1 if its lower one).  Before each force
-   pass an engine's stream waits until every neighbour finished the previous
-   pass.  Link before the first frame; every band must step in lockstep.
+   word 0 if I am its upper neighbour, 1 if its lower one) with the passes it
+   completed.  A force pass may read its halo / overwrite the neighbour's
+   only after every neighbour finished the previous pass.  Fast
+   collision-free bands with fused normals do this inside the step kernel:
+   only the warps of the seam chunk rows wait (spinning on the flag words),
+   the launch's last block signals, and frames replay a CUDA graph like a
+   single engine's.  Otherwise (CS_FLAG_MEMOP_SEAM, fixed arithmetic, split
+   normals, obstacles) the stream waits on / writes the flag words around
+   each pass.  Link before the first frame; every band must step in lockstep.
    With an obstacle (replicated per band) a frame has three handshakes:
    post-step rows -> detect -> "detect done" -> respond -> post-respond rows.
    Drive each band from its own CUDA context (one process per GPU): inside

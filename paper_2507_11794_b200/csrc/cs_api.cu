@@ -134,22 +134,20 @@ struct cs_engine {
     };
     bool banded = false;
     Link up, dn;
-    // flag block (grid engines): words [0, 2 sxn) interleave from_up /
-    // from_dn per strip (the neighbours write them; the memop handshake uses
-    // words 0 and 1), word 2 sxn the persistent kernel's error word, per-chunk
-    // pass marks from done_off on
+    // flag words: [0] passes the upper neighbour finished, [1] the lower one's
+    // (written by them), [2] passes this band finished (device counter of
+    // the in-kernel handshake), [3] blocks done in the running launch, [4]
+    // the in-kernel handshake's error word
     uint32_t *hflags = nullptr;
-    int64_t flag_words = 0;
-    int sxn = 0, done_off = 0;
     uint32_t passes = 0;         // force passes this engine issued
-    bool persist_used = false;   // a persistent launch ran (its error word is live)
-    // the persistent multi-pass kernel (k_pair3_persist) serves every
-    // multi-frame step of a fast, collision-free grid engine with fused
-    // normals, and every frame of such a row band (the seam handshake is
-    // then inside the kernel)
-    bool persist_ok() const {
-        return grid && strip && (flags & CS_FLAG_PAIRED) && !fixed && !fp64 && !has_obstacle &&
-               substeps == 1 && fuse_normals() && !(flags & CS_FLAG_NO_PERSIST) && hflags;
+    // Fast collision-free bands with fused normals do the seam handshake
+    // inside k_pair3 (seam warps wait, the last block signals): frames are
+    // graph-captured like a single engine's.  Otherwise (fixed arithmetic,
+    // split normals, obstacles, CS_FLAG_MEMOP_SEAM) the stream waits on /
+    // writes the flag words around each pass.
+    bool seam_in_kernel() const {
+        return banded && grid && strip && (flags & CS_FLAG_PAIRED) && !fixed && !has_obstacle &&
+               fuse_normals() && !(flags & CS_FLAG_MEMOP_SEAM);
     }
     StepParams sp{};
     CsrParams cp{};
@@ -293,9 +291,20 @@ static void drop_graphs(cs_engine *h) {
 // ---------------------------------------------------------------------------
 // passes
 // ---------------------------------------------------------------------------
+static HaloDst halo_dst(const cs_engine *h, int dst);
+
 static void pass_force_integrate(cs_engine *h, bool fuse_normals = false) {
     for (int s = 0; s < h->substeps; ++s) {
         const int src = h->cur, dst = 1 - h->cur;
+        if (h->seam_in_kernel()) {  // a row band: peer stores + seam handshake in the kernel
+            const HaloDst hd = halo_dst(h, dst);
+            launch_strip_step(h->sp, false, fuse_normals && s == 0, (const float *)h->state[src],
+                              (float *)h->state[dst], h->pinbits,
+                              h->has_ext ? (const float *)h->ext : nullptr, (float *)h->normals,
+                              h->st, true, &hd);
+            h->cur = dst;
+            continue;
+        }
         if (h->fp64) {
             launch_csr_step_f64(h->cp, (const double *)h->state[src], (double *)h->state[dst],
                                 h->csr_off, h->csr_nbr, h->csr_kind, h->csr_rest64, h->mass64,
@@ -492,75 +501,21 @@ static HaloDst halo_dst(const cs_engine *h, int dst) {
     };
     fill(h->up, d.up);
     fill(h->dn, d.dn);
+    if (h->seam_in_kernel()) {
+        d.flags = h->hflags;
+        d.to_up = h->up.on ? h->up.remote_flag : nullptr;
+        d.to_dn = h->dn.on ? h->dn.remote_flag : nullptr;
+    }
     return d;
 }
 
-// The persistent scheme's equivalent of halo_wait: until every strip of
-// each linked neighbour has finished `target` passes (its seam rows of our
-// current state landed).  One small block; gives up after the kernel's time
-// limit and flags the error word.
-__global__ void k_band_wait(const uint32_t *flags, int sxn, int up, int dn, uint32_t target,
-                            uint32_t *err) {
-    const uint64_t t0 = clock64();
-    for (int i = threadIdx.x; i < 2 * sxn; i += blockDim.x) {
-        if (!((i & 1) ? dn : up)) continue;
-        for (;;) {
-            uint32_t v;
-            asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(flags + i) : "memory");
-            if ((int32_t)(v - target) >= 0) break;
-            if (*(volatile uint32_t *)err) return;
-            if (clock64() - t0 > (int64_t)40e9) {  // ~20 s at 2 GHz
-                atomicExch(err, 1u);
-                return;
-            }
-            __nanosleep(256);
-        }
-    }
-}
-
-static int band_wait(cs_engine *h);
-
-static int persist_launch(cs_engine *h, int32_t frames) {
-    PersistLaunch L;
-    L.buf[0] = (const float *)h->state[0];
-    L.buf[1] = (const float *)h->state[1];
-    L.cur0 = h->cur;
-    L.passes = frames;
-    L.base = h->passes;
-    L.flags = h->hflags;
-    L.flag_words = h->flag_words;
-    L.sxn = h->sxn;
-    L.done_off = h->done_off;
-    HaloDst hd[2];
-    if (h->banded) {
-        hd[0] = halo_dst(h, 0);
-        hd[1] = halo_dst(h, 1);
-        L.halo[0] = &hd[0];
-        L.halo[1] = &hd[1];
-        L.to_up = h->up.on ? h->up.remote_flag : nullptr;
-        L.to_dn = h->dn.on ? h->dn.remote_flag : nullptr;
-    }
-    const cudaError_t e = launch_pair3_persist(h->sp, L, h->pinbits,
-                                               h->has_ext ? (const float *)h->ext : nullptr,
-                                               (float *)h->normals, h->st);
-    if (e != cudaSuccess)
-        return fail(CS_E_CUDA, std::string("persistent step launch: ") + cudaGetErrorString(e));
-    h->persist_used = true;
-    h->passes += (uint32_t)frames;
-    if (frames & 1) h->cur ^= 1;
-    h->forces_valid = true;
-    h->normals_stale = true;  // fused normals trail by one frame
-    h->frames += frames;
-    return 0;
-}
-
-// a persistent launch that hit its wait limit (a neighbour never came)
-static int persist_check(cs_engine *h) {
-    if (!h->persist_used) return 0;
+// the in-kernel handshake gave up waiting for a neighbour (error word)
+static int seam_check(cs_engine *h) {
+    if (!h->seam_in_kernel()) return 0;
     uint32_t e = 0;
-    CK(cudaMemcpyAsync(&e, h->hflags + 2 * h->sxn, sizeof(e), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaMemcpyAsync(&e, h->hflags + 4, sizeof(e), cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
-    if (e) return fail(CS_E_CUDA, "row-band handshake timed out (a neighbour band stopped stepping)");
+    if (e) return fail(CS_E_CUDA, "row-band seam handshake timed out (a neighbour band stopped stepping)");
     return 0;
 }
 
@@ -617,19 +572,9 @@ static int banded_frame(cs_engine *h) {
     return 0;
 }
 
-static int band_wait(cs_engine *h) {
-    if (!h->banded) return 0;
-    if (!h->persist_ok()) return halo_wait(h);
-    k_band_wait<<<1, 128, 0, h->st>>>(h->hflags, h->sxn, h->up.on ? 1 : 0, h->dn.on ? 1 : 0,
-                                      h->passes, h->hflags + 2 * h->sxn);
-    CK(cudaGetLastError());
-    h->persist_used = true;
-    return 0;
-}
-
 static void flush_normals(cs_engine *h) {
     if (h->normals_stale) {
-        if (h->banded) band_wait(h);  // the neighbours' last pass completes our halo
+        if (h->banded) halo_wait(h);  // the neighbours' last pass completes our halo
         pass_normals(h);
         h->normals_stale = false;
     }
@@ -871,15 +816,6 @@ static int build(cs_engine *h, const cs_desc *d) {
         }
     }
 
-    // ---- flag block (row bands, persistent kernel) ----
-    if (h->grid) {
-        h->sxn = (int)((h->nx + 59) / 60);
-        h->done_off = 2 * h->sxn + 32;
-        h->flag_words = h->done_off + (int64_t)h->sxn * h->rows;
-        CK(dalloc(&h->hflags, h->flag_words));
-        CK(cudaMemsetAsync(h->hflags, 0, h->flag_words * sizeof(uint32_t), h->st));
-    }
-
     // ---- collision buffers + broad phase (engine.py:218-230) ----
     CK(dalloc(&h->stats, 4 + 2 * cs_engine::kRing));
     CK(cudaMemsetAsync(h->stats, 0, (4 + 2 * cs_engine::kRing) * sizeof(unsigned long long), h->st));
@@ -985,10 +921,7 @@ extern "C" int cs_create(const cs_desc *d, cs_engine **out) {
 // ---------------------------------------------------------------------------
 extern "C" int cs_step(cs_engine *h, int32_t frames) {
     if (!h) return fail(CS_E_INVALID, "null engine");
-    if (frames <= 0) return 0;
-    if (h->persist_ok() && (h->banded || frames >= 2))
-        return persist_launch(h, frames);  // one launch, the seam handshake inside it
-    if (h->banded) {  // per-pass handshake values change every frame: no graph
+    if (h->banded && !h->seam_in_kernel()) {  // stream handshake values change every frame: no graph
         for (int32_t f = 0; f < frames; ++f) {
             if (int r = banded_frame(h)) return r;
             h->frames++;
@@ -1016,6 +949,7 @@ extern "C" int cs_step(cs_engine *h, int32_t frames) {
             launch_frame(h);
             CK(cudaGetLastError());
         }
+        if (h->banded) h->passes += (uint32_t)h->substeps;  // replayed in-kernel handshakes
         h->frames++;
     }
     return 0;
@@ -1045,7 +979,8 @@ extern "C" int cs_record(cs_engine *h, int32_t frames, float *host_out) {
         if (int r = cs_step(h, 1)) return r;
         // a row band's halo rows of the new state are the neighbours' peer
         // stores: wait for their pass, as cs_read does, before copying
-        if (int r = band_wait(h)) return r;
+        if (h->banded)
+            if (int r = halo_wait(h)) return r;
         CK(cudaEventRecord(h->ev_frame[k], h->st));
         CK(cudaStreamWaitEvent(h->copy_st, h->ev_frame[k], 0));
         k_planes_to_aos<float><<<nb(h->N), 256, 0, h->copy_st>>>(
@@ -1167,7 +1102,7 @@ extern "C" int cs_frame_hits(cs_engine *h, int64_t frame, int64_t *hits, int64_t
 extern "C" int cs_synchronize(cs_engine *h) {
     if (!h) return fail(CS_E_INVALID, "null engine");
     CK(cudaStreamSynchronize(h->st));
-    return persist_check(h);
+    return seam_check(h);
 }
 
 extern "C" int cs_stream(cs_engine *h, void **stream) {
@@ -1183,7 +1118,7 @@ static int cs_read_impl(cs_engine *h, int32_t id, void *dst);
 extern "C" int cs_read(cs_engine *h, int32_t id, void *dst) {
     if (!h || !dst) return fail(CS_E_INVALID, "null argument");
     if (int r = cs_read_impl(h, id, dst)) return r;
-    return persist_check(h);
+    return seam_check(h);
 }
 static int cs_read_impl(cs_engine *h, int32_t id, void *dst) {
     const int64_t P = h->plane;
@@ -1194,7 +1129,9 @@ static int cs_read_impl(cs_engine *h, int32_t id, void *dst) {
         case CS_BUF_NORMALS:
         case CS_BUF_NORMALS_LAGGED: {
             if (id == CS_BUF_NORMALS) flush_normals(h);
-            if (int r = band_wait(h)) return r;  // halo rows of the current state landed
+            if (h->banded) {
+                if (int r = halo_wait(h)) return r;  // halo rows of the current state landed
+            }
             const void *base = (id == CS_BUF_NORMALS || id == CS_BUF_NORMALS_LAGGED) ? h->normals
                                : id == CS_BUF_PREV_POSITIONS ? h->state[1 - h->cur]
                                                              : h->state[h->cur];
@@ -1375,7 +1312,8 @@ extern "C" int cs_read_device(cs_engine *h, int32_t id, void *dst, void *stream)
         if (!h->fp64) return fail(CS_E_INVALID, "float64 buffers need a CS_FLAG_FP64 engine");
         want64 = true;
     }
-    if (int r = band_wait(h)) return r;  // halo rows of the current state landed
+    if (h->banded)
+        if (int r = halo_wait(h)) return r;  // halo rows of the current state landed
     if (int r = join(h, h->st, s)) return r;
     const unsigned g = nb(h->N);
     if (i32)
@@ -1418,7 +1356,8 @@ extern "C" int cs_write_device(cs_engine *h, int32_t id, const void *src, void *
     }
     if (src64 && !h->fp64) return fail(CS_E_INVALID, "float64 buffers need a CS_FLAG_FP64 engine");
     if (id == CS_BUF_POSITIONS || id == CS_BUF_VELOCITIES || src64) flush_normals(h);
-    if (int r = band_wait(h)) return r;
+    if (h->banded)
+        if (int r = halo_wait(h)) return r;
     if (int r = join(h, h->st, s)) return r;
     const unsigned g = nb(h->N);
     if (src64)
@@ -1459,9 +1398,8 @@ extern "C" int cs_state_buffers(cs_engine *h, void **state0, void **state1, uint
                                 int64_t *plane, int64_t *pitch) {
     if (!h) return fail(CS_E_INVALID, "null engine");
     if (!h->hflags) {
-        h->flag_words = 2;
-        CK(dalloc(&h->hflags, 2));
-        CK(cudaMemset(h->hflags, 0, 2 * sizeof(uint32_t)));
+        CK(dalloc(&h->hflags, 8));
+        CK(cudaMemset(h->hflags, 0, 8 * sizeof(uint32_t)));
     }
     if (state0) *state0 = h->state[0];
     if (state1) *state1 = h->state[1];
@@ -1512,7 +1450,7 @@ extern "C" int cs_set_halo_peers(cs_engine *h, int64_t row_lo, int64_t row_hi,
     h->sp.halo_dn_lo = h->dn.on ? (int)h->dn.src_row0 : INT_MAX;
     h->banded = true;
     h->passes = 0;
-    drop_graphs(h);
+    drop_graphs(h);  // frames now carry the peer stores (and the in-kernel handshake)
     return 0;
 }
 
@@ -1630,7 +1568,9 @@ extern "C" int cs_snapshot_render(const double *verts, const int32_t *tris, int6
 // snapshot_png from read_positions().astype(float64), without the readback).
 extern "C" int cs_positions_device(cs_engine *h, double *dev_out) {
     if (!h || !dev_out) return fail(CS_E_INVALID, "null argument");
-    if (int r = band_wait(h)) return r;
+    if (h->banded) {
+        if (int r = halo_wait(h)) return r;
+    }
     const int64_t nxx = h->grid ? h->nx : h->N;
     if (h->fp64)
         k_planes_to_aos64<double><<<nb(h->N), 256, 0, h->st>>>(

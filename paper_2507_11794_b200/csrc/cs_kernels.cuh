@@ -175,6 +175,14 @@ void launch_grid_step(const StepParams &p, bool fixed, const float *src, float *
 struct HaloDst {
     float *up[6];
     float *dn[6];
+    // the in-kernel seam handshake (k_pair3; null = the stream waits /
+    // signals around the kernel instead): this band's flag words -- [0]
+    // passes the upper neighbour completed, [1] the lower one's (both
+    // written by them), [2] passes this band completed (a device counter, so
+    // the frame is graph-capturable), [3] blocks finished in the running
+    // launch, [4] error word -- and the neighbours' words this band writes
+    uint32_t *flags = nullptr;
+    uint32_t *to_up = nullptr, *to_dn = nullptr;
 };
 void launch_strip_step(const StepParams &p, bool fixed, bool normals, const float *src,
                        float *dst, const uint32_t *pinbits, const float *ext, float *nrm,
@@ -187,24 +195,6 @@ void launch_push_rows(const float *src, int64_t plane, int pitch, int r0, int r1
                       float *const to[6], cudaStream_t st);
 void launch_pair_normals(const StepParams &p, const float *state, float *nrm, cudaStream_t st);
 int pair3_rows(const StepParams &p);
-// Persistent multi-pass launch of the fused fast kernel (cs_pair3.cu
-// k_pair3_persist): `passes` passes over buf[0] / buf[1] starting from
-// buf[cur0], every pass's chunks ordered by per-chunk flags in `flags` (the
-// engine's flag block, flag_words long); row bands add the neighbours' halo
-// planes (halo[d]: stores into the neighbours' buffer d) and flag words.
-struct PersistLaunch {
-    const float *buf[2];
-    int cur0 = 0, passes = 0;
-    uint32_t base = 0;
-    uint32_t *flags = nullptr;
-    int64_t flag_words = 0;
-    int sxn = 0, done_off = 0;
-    uint32_t *to_up = nullptr, *to_dn = nullptr;
-    const HaloDst *halo[2] = {nullptr, nullptr};
-};
-cudaError_t launch_pair3_persist(const StepParams &p, const PersistLaunch &L,
-                                 const uint32_t *pinbits, const float *ext, float *nrm,
-                                 cudaStream_t st);
 void launch_pair3_forces(const StepParams &p, const float *src, const uint32_t *pinbits,
                          int32_t *forces, cudaStream_t st);
 void launch_grid_forces(const StepParams &p, const float *src, int32_t *forces, cudaStream_t st);

@@ -256,7 +256,7 @@ class Engine:
                  pair_budget: int = DEFAULT_PAIR_BUDGET, *, precision: str = "fast",
                  graph: bool = True, stream=None, cell_size: float | None = None,
                  force_csr: bool = False, kernel: str = "pair", narrow: str = "batch",
-                 normals: str = "auto", persist: bool = True):
+                 normals: str = "auto", seam: str = "kernel"):
         if precision not in PRECISIONS:
             raise ValueError(f"precision must be one of {PRECISIONS}")
         self.mesh = mesh
@@ -352,8 +352,11 @@ class Engine:
             flags |= N.FLAG_WARP_NARROW
         if kernel == "pair":
             flags |= N.FLAG_PAIRED
-        if not persist:
-            flags |= N.FLAG_NO_PERSIST
+        if seam not in ("kernel", "stream"):
+            raise ValueError("seam must be 'kernel' (row-band handshake inside the step kernel, "
+                             "graph-replayed frames) or 'stream' (stream waits on flag words)")
+        if seam == "stream":
+            flags |= N.FLAG_MEMOP_SEAM
         d.flags = flags
         if stencil is not None:
             d.nx, d.ny = stencil[0], stencil[1]

@@ -144,12 +144,13 @@ def test_c3_drapes_finite_with_contacts_in_both_modes():
     assert abs(hits["fast"] - hits["fixed"]) / hits["fixed"] < 0.05
 
 
-@pytest.mark.parametrize("world,precision,n,normals,persist", [
-    (2, "fast", 160, "auto", True), (3, "fast", 161, "auto", True), (3, "fast", 130, "split", True),
-    (4, "fixed", 96, "auto", True), (2, "fast", 64, "fused", True), (3, "fast", 161, "auto", False),
-    (4, "fast", 300, "auto", True),
+@pytest.mark.parametrize("world,precision,n,normals,seam", [
+    (2, "fast", 160, "auto", "kernel"), (3, "fast", 161, "auto", "kernel"),
+    (3, "fast", 130, "split", "kernel"), (4, "fixed", 96, "auto", "kernel"),
+    (2, "fast", 64, "fused", "kernel"), (3, "fast", 161, "auto", "stream"),
+    (4, "fast", 300, "auto", "kernel"),
 ])
-def test_p2p_bands_bit_identical_to_one_engine(world, precision, n, normals, persist):
+def test_p2p_bands_bit_identical_to_one_engine(world, precision, n, normals, seam):
     """Row bands linked by peer stores inside the step kernel (the NVLink
     path of bench.py --gpus N), several bands on one device, each on its own
     stream: owned rows equal the single-engine run bit for bit (positions,
@@ -158,8 +159,9 @@ def test_p2p_bands_bit_identical_to_one_engine(world, precision, n, normals, per
     context, so this single-process test enqueues one frame per band and
     synchronises before the next (every wait is then already satisfied); the
     cross-process tests below exercise the real blocking handshake.  Fast
-    collision-free bands run the persistent kernel with the seam flags inside
-    it (persist=True); persist=False keeps the stream-memop handshake."""
+    collision-free bands do the handshake inside the step kernel (seam
+    warps wait, graph-replayed frames: seam="kernel"); seam="stream" keeps
+    the stream-memop handshake."""
     from paper_2507_11794_b200.bands import link_local
 
     k, c = stable_coefficients(NODE_MASS, CONTACT_DT)
@@ -167,7 +169,7 @@ def test_p2p_bands_bit_identical_to_one_engine(world, precision, n, normals, per
     whole = P.Engine(P.build_scene(P.ScenarioConfig("hanging", (n, n), dt=CONTACT_DT)).mesh,
                      params=params, precision=precision, normals=normals)
     bands = [BandedEngine(n, n, params, r, world, exchange="p2p", precision=precision,
-                          normals=normals, persist=persist) for r in range(world)]
+                          normals=normals, seam=seam) for r in range(world)]
     link_local(bands)
     whole.step_frames(30)
     for _ in range(30):
@@ -196,7 +198,7 @@ def test_p2p_link_validation():
         link_local(bands)
 
 
-@pytest.mark.parametrize("n,world,obstacle", [(192, 2, None), (192, 3, "nopersist"),
+@pytest.mark.parametrize("n,world,obstacle", [(192, 2, None), (192, 3, "stream"),
                                               (48, 2, "icosphere:3"), (60, 3, "uvsphere:40x40")])
 def test_ipc_linked_bands_across_processes(n, world, obstacle):
     """The multi-process link (CUDA IPC handles swapped over torch.distributed,

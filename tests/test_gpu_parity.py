@@ -324,27 +324,3 @@ def test_strided_batches_of_every_size_equal_warp_per_query(n):
     assert len(ca) > 100
     key = lambda c: c[np.lexsort((c[:, 1], c[:, 0]))]  # noqa: E731 (multiset order)
     np.testing.assert_array_equal(key(ca), key(cb))
-
-
-@pytest.mark.parametrize("shape", [(67, 130), (800, 96), (61, 2), (2048, 2048), (4096, 515)])
-def test_persistent_multi_frame_kernel_equals_per_frame_launches(shape):
-    """step_frames(K) of a fast collision-free engine runs ONE persistent
-    launch whose chunks are ordered by per-chunk flags (k_pair3_persist); it
-    must equal K per-frame graph replays bit for bit -- positions,
-    velocities, normals (lagged and current), with and without ext accel."""
-    sc = P.build_scene(P.ScenarioConfig("hanging", shape, dt=0.004))
-    a = P.Engine(sc.mesh, params=sc.params)
-    b = P.Engine(sc.mesh, params=sc.params, persist=False)
-    for e in (a, b):
-        e.step_frames(7)
-        e.step_frames(6)
-    for what in ("positions", "velocities", "normals_lagged", "normals", "previous_positions"):
-        np.testing.assert_array_equal(getattr(a, f"read_{what}")(), getattr(b, f"read_{what}")(),
-                                      err_msg=what)
-    ext = np.tile(np.float32([0.5, 0.0, -0.25]), (sc.mesh.num_nodes, 1))
-    for e in (a, b):
-        e.set_external_accel(ext)
-        e.step_frames(5)
-    np.testing.assert_array_equal(a.read_positions(), b.read_positions())
-    np.testing.assert_array_equal(a.read_velocities(), b.read_velocities())
-    a.synchronize()

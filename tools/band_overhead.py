@@ -41,13 +41,13 @@ def timed(fn):
     return a.elapsed_time(b) / k * 1e3
 
 
-def self_linked(world, persist):
+def self_linked(world, seam):
     """A middle band linked to a dummy neighbour; its remote flag words are
     its own, so every wait is satisfied by its own previous pass."""
     me = BandedEngine(4096, 4096, params, 1, world, stream=stream.cuda_stream, exchange="p2p",
-                      persist=persist)
+                      seam=seam)
     dummy = BandedEngine(4096, 4096, params, 1, world, stream=stream.cuda_stream, exchange="p2p",
-                         persist=persist)
+                         seam=seam)
     mine, info = me.buffers(), dummy.buffers()
     # link() aims the up signal at up.flags + 4 (the neighbour's from_dn) and
     # the down signal at down.flags + 0 (its from_up); shift both so they land
@@ -59,24 +59,15 @@ def self_linked(world, persist):
 
 
 out = []
-for world in (1, 2, 4, 8):
+for world in (2, 4, 8):
     rec = {"gpus": world}
-    for persist in (False, True):
-        tag = "persist" if persist else "per_frame"
-        if world == 1:
-            sc = P.baseline_scene("C5")
-            eng = P.Engine(sc.mesh, params=params, stream=stream.cuda_stream, persist=persist)
-            del sc
-            rec[f"sheet_{tag}_us"] = timed(lambda f: eng.step_frames(f))
-            eng.close()
-            continue
-        me = BandedEngine(4096, 4096, params, 1, world, stream=stream.cuda_stream,
-                          exchange="p2p", persist=persist)
-        rec["local_rows"] = me.local_rows
-        rec[f"plain_{tag}_us"] = timed(lambda f: me.engine.step_frames(f))
-        me.close()
-        me, dummy = self_linked(world, persist)
-        rec[f"linked_{tag}_us"] = timed(lambda f: me.step(f))
+    me = BandedEngine(4096, 4096, params, 1, world, stream=stream.cuda_stream, exchange="p2p")
+    rec["local_rows"] = me.local_rows
+    rec["plain_us"] = timed(lambda f: me.engine.step_frames(f))
+    me.close()
+    for seam in ("stream", "kernel"):
+        me, dummy = self_linked(world, seam)
+        rec[f"linked_{seam}_us"] = timed(lambda f: me.step(f))
         assert np.isfinite(me.owned_positions()).all()
         me.close()
         dummy.close()

@@ -6,11 +6,11 @@ gathered owned rows with a single engine, bit for bit.  This exercises the
 same IPC + peer-store + flag-handshake path bench.py --gpus N uses across
 GPUs (streams wait on flag words; no kernel waits on another).
 
-    timeout 300 python tools/ipc_bands_smoke.py [n] [world] [obstacle, e.g. icosphere:3 | nopersist]
+    timeout 300 python tools/ipc_bands_smoke.py [n] [world] [obstacle, e.g. icosphere:3 | stream]
 
-Collision-free bands run the persistent kernel (the seam flags inside the
-kernel, its warps spinning on the neighbour's flag words); "nopersist" keeps
-the stream-memop handshake.
+Collision-free bands do the seam handshake inside the step kernel (seam
+warps spin on the neighbour's flag words); "stream" keeps the stream-memop
+handshake.
 """
 import os
 import socket
@@ -24,7 +24,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 
-def _worker(rank, world, port, n, q, obstacle, persist=True):
+def _worker(rank, world, port, n, q, obstacle, seam="kernel"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
@@ -41,7 +41,7 @@ def _worker(rank, world, port, n, q, obstacle, persist=True):
         band = BandedEngine(n, n, params, rank, world, exchange="p2p", mesh=sc.mesh,
                             obstacle=sc.obstacle, pair_budget=10**13)
     else:
-        band = BandedEngine(n, n, params, rank, world, exchange="p2p", persist=persist)
+        band = BandedEngine(n, n, params, rank, world, exchange="p2p", seam=seam)
     band.link_ipc()
     frames = 120 if obstacle else 30
     band.step(frames)
@@ -74,15 +74,15 @@ def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 256
     world = int(sys.argv[2]) if len(sys.argv) > 2 else 2
     obstacle = sys.argv[3] if len(sys.argv) > 3 else None
-    persist = True
-    if obstacle == "nopersist":  # collision-free bands on the stream-memop handshake
-        obstacle, persist = None, False
+    seam = "kernel"
+    if obstacle == "stream":  # collision-free bands on the stream-memop handshake
+        obstacle, seam = None, "stream"
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q, obstacle, persist)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q, obstacle, seam)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
