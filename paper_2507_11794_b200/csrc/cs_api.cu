@@ -135,9 +135,9 @@ struct cs_engine {
     bool banded = false;
     Link up, dn;
     // flag words: [0] passes the upper neighbour finished, [1] the lower one's
-    // (written by them), [2] passes this band finished (device counter of
-    // the in-kernel handshake), [3] blocks done in the running launch, [4]
-    // the in-kernel handshake's error word
+    // (written by them); the in-kernel handshake's [2] / [5] passes whose
+    // upper / lower seam this band finished, [3] / [6] seam warps done in the
+    // running launch, [4] its error word (HaloDst::flags)
     uint32_t *hflags = nullptr;
     uint32_t passes = 0;         // force passes this engine issued
     // Fast collision-free bands with fused normals do the seam handshake

@@ -176,11 +176,12 @@ struct HaloDst {
     float *up[6];
     float *dn[6];
     // the in-kernel seam handshake (k_pair3; null = the stream waits /
-    // signals around the kernel instead): this band's flag words -- [0]
-    // passes the upper neighbour completed, [1] the lower one's (both
-    // written by them), [2] passes this band completed (a device counter, so
-    // the frame is graph-capturable), [3] blocks finished in the running
-    // launch, [4] error word -- and the neighbours' words this band writes
+    // signals around the kernel instead): this band's flag words -- [0] /
+    // [1] passes the upper / lower neighbour completed (written by them),
+    // [2] / [5] passes whose upper / lower seam this band completed (device
+    // counters, so the frame is graph-capturable), [3] / [6] seam warps done
+    // in the running launch, [4] error word -- and the neighbours' words
+    // this band writes
     uint32_t *flags = nullptr;
     uint32_t *to_up = nullptr, *to_dn = nullptr;
 };

@@ -9,7 +9,7 @@ system fences, no graph) but no cross-GPU latency and no neighbour skew.
 Compared with the same band stepped as a plain engine (one graph replay per
 frame).
 
-    python tools/band_overhead.py [frames]
+    python tools/band_overhead.py [frames] [worlds, e.g. 2,4,8]
 """
 import json
 import os
@@ -24,6 +24,7 @@ from paper_2507_11794_b200.bands import BandedEngine, HaloPlan
 from paper_2507_11794_b200.scenes import CONTACT_DT, NODE_MASS, stable_coefficients
 
 k = int(sys.argv[1]) if len(sys.argv) > 1 else 100
+worlds = [int(w) for w in sys.argv[2].split(",")] if len(sys.argv) > 2 else [2, 4, 8]
 kk, cc = stable_coefficients(NODE_MASS, CONTACT_DT)
 params = P.SimParams(dt=CONTACT_DT, stiffness=kk, damping=cc)
 stream = torch.cuda.Stream()
@@ -59,7 +60,7 @@ def self_linked(world, seam):
 
 
 out = []
-for world in (2, 4, 8):
+for world in worlds:
     rec = {"gpus": world}
     me = BandedEngine(4096, 4096, params, 1, world, stream=stream.cuda_stream, exchange="p2p")
     rec["local_rows"] = me.local_rows
