@@ -447,35 +447,53 @@ def c5_roofline(P, torch, stream, args):
 
 
 def band_projection(P, torch, stream, scene_params, k, frame_ms):
-    """Config 5 split in N row bands (bench.py --gpus N): one band's frame
-    (4096 x (4096/N + 4) rows incl. halos, the fused kernel) timed alone on
-    this GPU -- the compute part of an N-GPU frame.  The seam exchange (peer
-    stores of two rows each way inside the kernel + a stream flag handshake
-    per frame) is not in it, so the speed-up is a compute-only projection."""
-    from paper_2507_11794_b200.mesh import grid_band
+    """Config 5 split in N row bands (bench.py --gpus N), projected from one
+    GPU: a middle band (rank 1 of N: 4096 x (4096/N + 4) local rows) timed
+    alone, (a) as a plain engine (compute only) and (b) LINKED -- peer stores
+    of its seam rows into a neighbour band's buffers and the in-kernel seam
+    handshake every frame, with its remote flag words aimed at its own so
+    every wait is met by its own previous pass (tools/band_overhead.py).  (b)
+    carries the whole per-frame seam machinery; what it cannot carry is the
+    NVLink flag latency between two real GPUs, which only the seam warps
+    (shortened chunk rows) wait for."""
+    from paper_2507_11794_b200.bands import BandedEngine, HaloPlan
 
-    out = []
-    for gpus in (2, 4, 8):
-        rows = 4096 // gpus + 4
-        band = grid_band(4096, 4096, 0, rows, total_mass=0.05 * 4096 * 4096, pinned_rows="first")
-        band.positions = np.stack([band.positions[:, 0], -band.positions[:, 2],
-                                   np.zeros(len(band.positions))], axis=1)
-        eng = P.Engine(band, params=scene_params, stream=stream.cuda_stream)
-        eng.step_frames(3)
+    def timed(fn):
+        fn(3)
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         a.record(stream)
-        eng.step_frames(k)
+        fn(k)
         b.record(stream)
         torch.cuda.synchronize()
-        ms = a.elapsed_time(b) / k
-        eng.close()
-        out.append({"gpus": gpus, "band_rows": rows, "band_frame_ms": ms,
-                    "projected_speedup": frame_ms / ms})
+        return a.elapsed_time(b) / k
+
+    out = []
+    for gpus in (2, 4, 8):
+        me = BandedEngine(4096, 4096, scene_params, 1, gpus, stream=stream.cuda_stream,
+                          exchange="p2p")
+        rows = me.local_rows
+        plain = timed(lambda f: me.engine.step_frames(f))
+        me.close()
+        me = BandedEngine(4096, 4096, scene_params, 1, gpus, stream=stream.cuda_stream,
+                          exchange="p2p")
+        dummy = BandedEngine(4096, 4096, scene_params, 1, gpus, stream=stream.cuda_stream,
+                             exchange="p2p")
+        mine, info = me.buffers(), dummy.buffers()
+        me.link((dict(info, flags=mine["flags"] - 4), HaloPlan(4096, gpus, 0)),
+                (dict(info, flags=mine["flags"] + 4), HaloPlan(4096, gpus, 2)) if gpus > 2 else None)
+        linked = timed(lambda f: me.step(f))
+        me.close()
+        dummy.close()
+        out.append({"gpus": gpus, "band_rows": rows, "band_frame_ms": plain,
+                    "linked_band_frame_ms": linked, "projected_speedup": frame_ms / plain,
+                    "projected_speedup_with_handshake": frame_ms / linked})
     return {"bands": out,
-            "note": "compute only: one band's fused frame kernel timed alone on this GPU "
-                    "(rows incl. 2+2 halo rows); the per-frame seam exchange is not included"}
+            "note": "band_frame_ms: a middle band's frame alone (compute); linked_band_frame_ms: "
+                    "the same band with its seam peer stores and in-kernel handshake every frame "
+                    "(self-linked: no cross-GPU flag latency); speed-ups against the whole-sheet "
+                    "frame on this GPU"}
 
 
 def collision_cpu_baseline(scene, positions, seconds=20.0):
