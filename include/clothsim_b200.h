@@ -72,10 +72,15 @@ extern "C" {
 #define CS_FLAG_FUSE_NORMALS 1024u  /* grid path: fuse (the default at every
                                        size; kept for explicitness) */
 #define CS_FLAG_THREAD_NARROW 256u  /* collision narrow phase: one thread per
-                                       query (default: 32-query batches per
+                                       query (default: batched queries per
                                        warp, flattened over cells/candidates) */
 #define CS_FLAG_WARP_NARROW 2048u   /* collision narrow phase: one warp per
                                        query */
+#define CS_FLAG_SPLIT_NARROW 8192u  /* collision narrow phase: 32-query batches
+                                       per warp, cloth edges (pass A) and cloth
+                                       triangles (pass B) enumerated separately
+                                       (default: one fused enumeration per
+                                       cloth triangle serves both passes) */
 #define CS_FLAG_MEMOP_SEAM 4096u  /* row bands: the stream-memop seam handshake
                                        (cuStreamWaitValue32 / WriteValue32
                                        around each pass, no graph) even where

@@ -32,6 +32,7 @@ FLAG_SPLIT_NORMALS = 512
 FLAG_FUSE_NORMALS = 1024
 FLAG_WARP_NARROW = 2048
 FLAG_MEMOP_SEAM = 4096
+FLAG_SPLIT_NARROW = 8192
 
 BUF_POSITIONS, BUF_VELOCITIES, BUF_NORMALS, BUF_PREV_POSITIONS = 0, 1, 2, 3
 BUF_FORCES_RAW, BUF_ACCUMULATOR, BUF_COUNTS, BUF_EXT_ACCEL = 4, 5, 6, 7

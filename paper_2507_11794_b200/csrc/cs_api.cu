@@ -182,9 +182,9 @@ struct cs_engine {
     }
     int kernels_per_frame() const {
         int k = substeps;  // one fused force+integrate launch per substep
-        // detect: both passes in one launch (batched narrow phase) or two;
-        // respond closes the frame in its last block
-        if (has_obstacle) k += (bp.warp_per_query == 2 ? 1 : 2) + 1;
+        // detect: both passes in one launch (fused or batched narrow phase)
+        // or two; respond closes the frame in its last block
+        if (has_obstacle) k += (bp.warp_per_query >= 2 ? 1 : 2) + 1;
         if (!fuse_normals()) k += grid ? 1 : 2;  // normals (else fused into the strip kernel)
         return k;
     }
@@ -839,7 +839,37 @@ static int build(cs_engine *h, const cs_desc *d) {
             return fail(CS_E_CUDA, std::string("broad-phase build failed: ") +
                                        cudaGetErrorString(cudaGetLastError()));
         h->bp.warp_per_query = (d->flags & CS_FLAG_THREAD_NARROW) ? 0
-                               : (d->flags & CS_FLAG_WARP_NARROW) ? 1 : 2;
+                               : (d->flags & CS_FLAG_WARP_NARROW)  ? 1
+                               : (d->flags & CS_FLAG_SPLIT_NARROW) ? 2 : 3;
+        if (h->bp.warp_per_query == 3 && h->nc > 0) {
+            // every unique cloth edge owned by the lowest-index triangle that
+            // contains it: bit k of tri_own[t] = edge (tris[t][k], tris[t][k+1 mod 3])
+            const int64_t C = h->nc;
+            std::vector<uint8_t> own(C, 0);
+            if (h->grid) {  // generate_cloth_grid's order (mesh.py:296-305), closed form
+                const int64_t nx = h->nx, cw = nx - 1;
+                for (int64_t t = 0; t < C; ++t) {
+                    const int64_t cell = t >> 1, i = cell % cw, j = cell / cw;
+                    own[t] = (t & 1) ? (uint8_t)6u  // T1 (v10, v01, v11): top and right edges
+                                     : (uint8_t)(2u | (i == 0 ? 1u : 0u) | (j == 0 ? 4u : 0u));
+                }
+            } else {
+                std::vector<std::pair<uint64_t, int64_t>> e(3 * C);
+                for (int64_t t = 0; t < C; ++t)
+                    for (int k = 0; k < 3; ++k) {
+                        const uint32_t a = (uint32_t)d->tris[3 * t + k];
+                        const uint32_t b = (uint32_t)d->tris[3 * t + (k + 1) % 3];
+                        const uint64_t key = ((uint64_t)std::min(a, b) << 32) | std::max(a, b);
+                        e[3 * t + k] = {key, 3 * t + k};
+                    }
+                std::sort(e.begin(), e.end());
+                for (size_t i = 0; i < e.size(); ++i)
+                    if (i == 0 || e[i].first != e[i - 1].first)
+                        own[e[i].second / 3] |= (uint8_t)(1u << (e[i].second % 3));
+            }
+            CK(dalloc(&h->bp.tri_own, C));
+            CK(cudaMemcpy(h->bp.tri_own, own.data(), C, cudaMemcpyHostToDevice));
+        }
         if (h->fp64) {
             CK(dalloc(&h->corners64, 9 * h->nt));
             CK(dalloc(&h->onormals64, 3 * h->nt));

@@ -362,6 +362,7 @@ int build_broadphase(BroadPhase &bp, const float *d_corners, int64_t nt, const f
 }
 
 void free_broadphase(BroadPhase &bp) {
+    cudaFree(bp.tri_own);
     cudaFree(bp.cell_be);
     cudaFree(bp.ref_box);
     cudaFree(bp.cell_begin);
@@ -848,6 +849,9 @@ constexpr int BATCH_WARPS = CS_DETECT_BATCH_WARPS;  // warps per narrow-phase bl
 #ifndef CS_DETECT_STRIDED
 #define CS_DETECT_STRIDED 1
 #endif
+#ifndef CS_DETECT_MINB
+#define CS_DETECT_MINB 8  // <= 64 registers, 32 resident warps per SM (strided queries: C3 frame -3%)
+#endif
 struct QuerySlot {
     float v[3][3];
     float lo[3], hi[3];   // query box (PASS 0: padded segment box; PASS 1: tri box +- 2 pad)
@@ -922,14 +926,13 @@ struct BatchShared {
     uint8_t qmeta[BATCH_WARPS][QCAP];  // query slot << 2 | edge slot
 };
 
-template <int PASS>
+template <int PASS, bool PACKED>
 __device__ __forceinline__ void detect_batch(BatchShared &S, int64_t blk, const CollideArgs &A,
                                              const GridDesc &g, const uint2 *__restrict__ cbe,
                                              const float4 *__restrict__ rbox,
                                              const float *__restrict__ corners,
                                              const float *__restrict__ normals,
-                                             const int32_t *__restrict__ items, int64_t nq, int qb,
-                                             bool packed) {
+                                             const int32_t *__restrict__ items, int64_t nq, int qb) {
     auto &slots = S.slots;
     auto &qtri = S.qtri;
     auto &qmeta = S.qmeta;
@@ -1010,10 +1013,14 @@ __device__ __forceinline__ void detect_batch(BatchShared &S, int64_t blk, const 
     const uint32_t cincl = warp_incl_scan(ncell);
     const uint32_t ctotal = __shfl_sync(0xffffffffu, cincl, 31);
     for (uint32_t c0 = 0; c0 < ctotal; c0 += 32) {
-        // this lane's (query, cell) pair
+        // this lane's (query, cell) pair; what a candidate lane needs of its
+        // owner cell goes out in three shuffles: `rb` (the cell's first
+        // reference minus its first flattened index: ref = rb + t), the cell
+        // coordinates packed 10:10:10 (every axis <= 1024 cells: PACKED) or
+        // its key, and the query slot
         const uint32_t c = c0 + lane;
-        int oq = 0, cx = 0, cy = 0, cz = 0;
-        uint32_t beg = 0, cnt = 0;
+        int oq = 0;
+        uint32_t cell = 0, beg = 0, cnt = 0;
         {
             const int o = warp_owner(cincl, c);
             const uint32_t oincl = __shfl_sync(0xffffffffu, cincl, o);
@@ -1021,44 +1028,46 @@ __device__ __forceinline__ void detect_batch(BatchShared &S, int64_t blk, const 
             if (c < ctotal) {
                 const QuerySlot &Q = slots[w][o];
                 const int local = (int)(c - (oincl - on));
-                cx = Q.a[0] + local % Q.ex;
-                cy = Q.a[1] + (local / Q.ex) % Q.ey;
-                cz = Q.a[2] + local / (Q.ex * Q.ey);
-                const uint2 r = cbe[g.key(cx, cy, cz)];
+                const int cx = Q.a[0] + local % Q.ex;
+                const int cy = Q.a[1] + (local / Q.ex) % Q.ey;
+                const int cz = Q.a[2] + local / (Q.ex * Q.ey);
+                const uint32_t key = g.key(cx, cy, cz);
+                const uint2 r = cbe[key];
                 beg = r.x;
                 cnt = r.y - r.x;
                 oq = o;
+                cell = PACKED ? (uint32_t)cx | ((uint32_t)cy << 10) | ((uint32_t)cz << 20) : key;
             }
         }
         const uint32_t incl = warp_incl_scan(cnt);
         const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t rbase = beg - (incl - cnt);
         for (uint32_t t0 = 0; t0 < total; t0 += 32) {
             const uint32_t t = t0 + lane;
             const int o = warp_owner(incl, t);
-            const uint32_t ob = __shfl_sync(0xffffffffu, beg, o);
-            const uint32_t oi = __shfl_sync(0xffffffffu, incl, o);
-            const uint32_t oc = __shfl_sync(0xffffffffu, cnt, o);
-            const int ox = __shfl_sync(0xffffffffu, cx, o);
-            const int oy = __shfl_sync(0xffffffffu, cy, o);
-            const int oz = __shfl_sync(0xffffffffu, cz, o);
+            const uint32_t orb = __shfl_sync(0xffffffffu, rbase, o);
+            const uint32_t ocell = __shfl_sync(0xffffffffu, cell, o);
             const int qq = __shfl_sync(0xffffffffu, oq, o);
             bool ok = t < total;
             uint32_t tri = 0;
             if (ok) {
                 const QuerySlot &Q = slots[w][qq];
-                const int64_t ref = ob + (t - (oi - oc));
-                const float4 b0 = rbox[2 * ref], b1 = rbox[2 * ref + 1];
+                const uint32_t ref = orb + t;
+                const float4 b0 = rbox[2 * (int64_t)ref], b1 = rbox[2 * (int64_t)ref + 1];
                 tri = __float_as_uint(b0.w);
                 const float tlo[3] = {b0.x, b0.y, b0.z}, thi[3] = {b1.x, b1.y, b1.z};
                 // box test, then dedup: the minimum corner of the intersection
                 // lies in this cell
-                if (packed) {
+                if (PACKED) {
                     const uint32_t tc = __float_as_uint(b1.w);
                     ok = box_overlap(Q.lo, Q.hi, tlo, thi) &&
-                         max(Q.a[0], (int)(tc & 1023u)) == ox &&
-                         max(Q.a[1], (int)((tc >> 10) & 1023u)) == oy &&
-                         max(Q.a[2], (int)(tc >> 20)) == oz;
+                         (uint32_t)max(Q.a[0], (int)(tc & 1023u)) == (ocell & 1023u) &&
+                         (uint32_t)max(Q.a[1], (int)((tc >> 10) & 1023u)) == ((ocell >> 10) & 1023u) &&
+                         (uint32_t)max(Q.a[2], (int)(tc >> 20)) == (ocell >> 20);
                 } else {
+                    const int ox = (int)(ocell % (uint32_t)g.dims[0]);
+                    const int oy = (int)((ocell / (uint32_t)g.dims[0]) % (uint32_t)g.dims[1]);
+                    const int oz = (int)(ocell / ((uint32_t)g.dims[0] * (uint32_t)g.dims[1]));
                     ok = box_overlap(Q.lo, Q.hi, tlo, thi) &&
                          g.cell_of(fmaxf(Q.lo[0], tlo[0]), 0) == ox &&
                          g.cell_of(fmaxf(Q.lo[1], tlo[1]), 1) == oy &&
@@ -1094,12 +1103,285 @@ __device__ __forceinline__ void detect_batch(BatchShared &S, int64_t blk, const 
     count_hits(A.frame_hits, hits);
 }
 
+// ---------------------------------------------------------------------------
+// Fused narrow phase (default, narrow="tri"): ONE candidate enumeration per
+// cloth triangle serves both reference passes.  The batched mapping above
+// enumerates grid candidates twice -- once per cloth edge (pass A) and once
+// per cloth triangle (pass B) -- although a cloth edge's padded box lies
+// inside its triangle's box padded by 2 pad.  Here every unique cloth edge
+// is owned by the lowest-index triangle containing it (tri_own: 3 bits per
+// triangle, built with the engine), and each surviving (cloth triangle,
+// obstacle triangle) candidate is expanded into
+//   * pass A items: each owned edge, oriented (lower node, higher node) as in
+//     unique_edges, whose padded box meets the obstacle triangle's box
+//     (kernels.py:55-78) -- the reference's own prefilter, exactly;
+//   * pass B items: each obstacle edge 3t+slot whose padded box meets the
+//     cloth triangle's box.
+// The candidate superset is the same as pass B's (the triangle query box),
+// so every pair the reference's prefilter keeps is tested exactly once; the
+// predicate, offsets, accumulation and hit ownership are those of the
+// other mappings (hits and integer accumulators identical).
+// ---------------------------------------------------------------------------
+struct TriSlot {
+    float v[3][3];
+    float lo[3], hi[3];    // query box: cloth triangle box +- 2 pad
+    float clo[3], chi[3];  // unpadded cloth triangle box (pass B's edge-box test)
+    int64_t nid[3];
+    int a[3], ex, ey;      // first cell and extents of the cell range
+    uint32_t own;          // owned-edge mask (edge k = nodes k, k+1 mod 3)
+};
+
+constexpr int QCAP_T = 224;  // < 32 left + 32 lanes x 6 items
+
+struct TriShared {
+    TriSlot slots[BATCH_WARPS][32];
+    uint32_t qtri[BATCH_WARPS][QCAP_T];
+    uint8_t qmeta[BATCH_WARPS][QCAP_T];  // query slot << 3 | kind (0-2: edge k; 3-5: slot)
+};
+
+// one item: pass A (kind 0-2, the query's edge `kind`) or pass B (kind 3-5,
+// obstacle edge slot kind-3) of query Q against obstacle triangle `tri`
+__device__ __forceinline__ uint32_t tri_item(const CollideArgs &A, const TriSlot &Q, uint32_t tri,
+                                             int kind, const float *__restrict__ corners,
+                                             const float *__restrict__ normals) {
+    const float *cr = corners + 9 * (int64_t)tri;
+    const float *nrm = normals + 3 * (int64_t)tri;
+    float pt[3];
+    if (kind < 3) {
+        const int k1 = kind == 2 ? 0 : kind + 1;
+        const bool lo_first = Q.nid[kind] < Q.nid[k1];
+        const int ia = lo_first ? kind : k1, ib = lo_first ? k1 : kind;
+        float st[3], en[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            st[d] = Q.v[ia][d];
+            en[d] = Q.v[ib][d];
+        }
+        if (!seg_tri(st, en, cr, cr + 3, cr + 6, A.eps, pt)) return 0;
+        const float sa = dot3x(fsub(st[0], pt[0]), fsub(st[1], pt[1]), fsub(st[2], pt[2]), nrm[0],
+                               nrm[1], nrm[2]);
+        const float sb = dot3x(fsub(en[0], pt[0]), fsub(en[1], pt[1]), fsub(en[2], pt[2]), nrm[0],
+                               nrm[1], nrm[2]);
+        const float sign = np_max(sa, sb) >= 0.f ? 1.f : -1.f;
+        const float on[3] = {fmul(nrm[0], sign), fmul(nrm[1], sign), fmul(nrm[2], sign)};
+        accumulate(A, Q.nid[ia], st, pt, on, tri);
+        accumulate(A, Q.nid[ib], en, pt, on, tri);
+        return owned_hit(A, Q.nid[ia]);
+    }
+    const int slot = kind - 3;
+    const float *st = cr + 3 * slot;
+    const float *en = cr + 3 * (slot == 2 ? 0 : slot + 1);
+    float v[3][3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) v[k][d] = Q.v[k][d];
+    if (!seg_tri(st, en, v[0], v[1], v[2], A.eps, pt)) return 0;
+    const float t0s = dot3x(fsub(v[0][0], pt[0]), fsub(v[0][1], pt[1]), fsub(v[0][2], pt[2]), nrm[0],
+                            nrm[1], nrm[2]);
+    const float t1s = dot3x(fsub(v[1][0], pt[0]), fsub(v[1][1], pt[1]), fsub(v[1][2], pt[2]), nrm[0],
+                            nrm[1], nrm[2]);
+    const float t2s = dot3x(fsub(v[2][0], pt[0]), fsub(v[2][1], pt[1]), fsub(v[2][2], pt[2]), nrm[0],
+                            nrm[1], nrm[2]);
+    const float sign = fadd(fadd(t0s, t1s), t2s) >= 0.f ? 1.f : -1.f;
+    const float on[3] = {fmul(nrm[0], sign), fmul(nrm[1], sign), fmul(nrm[2], sign)};
+    accumulate(A, Q.nid[0], v[0], pt, on, tri);
+    accumulate(A, Q.nid[1], v[1], pt, on, tri);
+    accumulate(A, Q.nid[2], v[2], pt, on, tri);
+    return owned_hit(A, min(Q.nid[0], min(Q.nid[1], Q.nid[2])));
+}
+
+template <bool PACKED>
+__device__ __forceinline__ void detect_tri(TriShared &S, int64_t blk, const CollideArgs &A,
+                                           const GridDesc &g, const uint2 *__restrict__ cbe,
+                                           const float4 *__restrict__ rbox,
+                                           const float *__restrict__ corners,
+                                           const float *__restrict__ normals,
+                                           const int32_t *__restrict__ tris,
+                                           const uint8_t *__restrict__ tri_own, int64_t nq, int qb) {
+    auto &slots = S.slots;
+    auto &qtri = S.qtri;
+    auto &qmeta = S.qmeta;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    // strided queries (as detect_batch): query = lane * warps + warp
+    const int64_t nw = (nq + qb - 1) / qb;
+    const int64_t wi = blk * BATCH_WARPS + w;
+    const int64_t q = wi < nw ? (int64_t)lane * nw + wi : nq;
+    TriSlot &my = slots[w][lane];
+    uint32_t ncell = 0;
+    if (lane < qb && q < nq) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            my.nid[k] = tris[3 * q + k];
+            load_pos(A, my.nid[k], my.v[k]);
+        }
+        my.own = tri_own[q];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            my.clo[d] = fminf(fminf(my.v[0][d], my.v[1][d]), my.v[2][d]);
+            my.chi[d] = fmaxf(fmaxf(my.v[0][d], my.v[1][d]), my.v[2][d]);
+            my.lo[d] = my.clo[d] - 2.0f * A.pad;
+            my.hi[d] = my.chi[d] + 2.0f * A.pad;
+        }
+        if (g.overlaps(my.lo, my.hi)) {
+            int a[3], b[3];
+            g.cell_range(my.lo, my.hi, a, b);
+            my.a[0] = a[0];
+            my.a[1] = a[1];
+            my.a[2] = a[2];
+            my.ex = b[0] - a[0] + 1;
+            my.ey = b[1] - a[1] + 1;
+            ncell = (uint32_t)(my.ex * my.ey * (b[2] - a[2] + 1));
+        }
+    }
+    __syncwarp();
+    uint32_t hits = 0;
+    int qn = 0;  // queued items (warp-uniform)
+    auto drain = [&](int keep) {  // run the predicate on full warps of queued items
+        while (qn > keep) {
+            const int take = qn - keep < 32 ? qn - keep : 32;
+            __syncwarp();
+            if (lane < take) {
+                const int k = qn - take + lane;
+                const uint8_t meta = qmeta[w][k];
+                hits += tri_item(A, slots[w][meta >> 3], qtri[w][k], meta & 7, corners, normals);
+            }
+            qn -= take;
+            __syncwarp();
+        }
+    };
+    auto push = [&](bool want, uint32_t tri, int qs, int kind) {
+        const uint32_t m = __ballot_sync(0xffffffffu, want);
+        if (want) {
+            const int k = qn + __popc(m & lt_mask);
+            qtri[w][k] = tri;
+            qmeta[w][k] = (uint8_t)((qs << 3) | kind);
+        }
+        qn += __popc(m);
+    };
+    const uint32_t cincl = warp_incl_scan(ncell);
+    const uint32_t ctotal = __shfl_sync(0xffffffffu, cincl, 31);
+    for (uint32_t c0 = 0; c0 < ctotal; c0 += 32) {
+        const uint32_t c = c0 + lane;
+        int oq = 0;
+        uint32_t cell = 0, beg = 0, cnt = 0;
+        {
+            const int o = warp_owner(cincl, c);
+            const uint32_t oincl = __shfl_sync(0xffffffffu, cincl, o);
+            const uint32_t on = __shfl_sync(0xffffffffu, ncell, o);
+            if (c < ctotal) {
+                const TriSlot &Q = slots[w][o];
+                const int local = (int)(c - (oincl - on));
+                const int cx = Q.a[0] + local % Q.ex;
+                const int cy = Q.a[1] + (local / Q.ex) % Q.ey;
+                const int cz = Q.a[2] + local / (Q.ex * Q.ey);
+                const uint32_t key = g.key(cx, cy, cz);
+                const uint2 r = cbe[key];
+                beg = r.x;
+                cnt = r.y - r.x;
+                oq = o;
+                cell = PACKED ? (uint32_t)cx | ((uint32_t)cy << 10) | ((uint32_t)cz << 20) : key;
+            }
+        }
+        const uint32_t incl = warp_incl_scan(cnt);
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t rbase = beg - (incl - cnt);
+        for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+            const uint32_t t = t0 + lane;
+            const int o = warp_owner(incl, t);
+            const uint32_t orb = __shfl_sync(0xffffffffu, rbase, o);
+            const uint32_t ocell = __shfl_sync(0xffffffffu, cell, o);
+            const int qq = __shfl_sync(0xffffffffu, oq, o);
+            bool ok = t < total;
+            uint32_t tri = 0;
+            float tlo[3] = {0.f, 0.f, 0.f}, thi[3] = {0.f, 0.f, 0.f};
+            if (ok) {
+                const TriSlot &Q = slots[w][qq];
+                const uint32_t ref = orb + t;
+                const float4 b0 = rbox[2 * (int64_t)ref], b1 = rbox[2 * (int64_t)ref + 1];
+                tri = __float_as_uint(b0.w);
+                tlo[0] = b0.x; tlo[1] = b0.y; tlo[2] = b0.z;
+                thi[0] = b1.x; thi[1] = b1.y; thi[2] = b1.z;
+                if (PACKED) {
+                    const uint32_t tc = __float_as_uint(b1.w);
+                    ok = box_overlap(Q.lo, Q.hi, tlo, thi) &&
+                         (uint32_t)max(Q.a[0], (int)(tc & 1023u)) == (ocell & 1023u) &&
+                         (uint32_t)max(Q.a[1], (int)((tc >> 10) & 1023u)) == ((ocell >> 10) & 1023u) &&
+                         (uint32_t)max(Q.a[2], (int)(tc >> 20)) == (ocell >> 20);
+                } else {
+                    const int ox = (int)(ocell % (uint32_t)g.dims[0]);
+                    const int oy = (int)((ocell / (uint32_t)g.dims[0]) % (uint32_t)g.dims[1]);
+                    const int oz = (int)(ocell / ((uint32_t)g.dims[0] * (uint32_t)g.dims[1]));
+                    ok = box_overlap(Q.lo, Q.hi, tlo, thi) &&
+                         g.cell_of(fmaxf(Q.lo[0], tlo[0]), 0) == ox &&
+                         g.cell_of(fmaxf(Q.lo[1], tlo[1]), 1) == oy &&
+                         g.cell_of(fmaxf(Q.lo[2], tlo[2]), 2) == oz;
+                }
+            }
+            // pass A: the query's owned edges whose padded box meets the
+            // obstacle triangle's box (kernels.py:55-78)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                bool e_ok = ok;
+                if (e_ok) {
+                    const TriSlot &Q = slots[w][qq];
+                    e_ok = (Q.own >> k) & 1u;
+                    if (e_ok) {
+                        const int k1 = k == 2 ? 0 : k + 1;
+                        float elo[3], ehi[3];
+#pragma unroll
+                        for (int d = 0; d < 3; ++d) {
+                            elo[d] = fsub(fminf(Q.v[k][d], Q.v[k1][d]), A.pad);
+                            ehi[d] = fadd(fmaxf(Q.v[k][d], Q.v[k1][d]), A.pad);
+                        }
+                        e_ok = box_overlap(elo, ehi, tlo, thi);
+                    }
+                }
+                push(e_ok, tri, qq, k);
+            }
+            // pass B: obstacle edges 3t+slot whose padded box meets the cloth
+            // triangle's box
+            const float *cr = corners + 9 * (int64_t)tri;
+#pragma unroll
+            for (int slot = 0; slot < 3; ++slot) {
+                bool e_ok = ok;
+                if (e_ok) {
+                    const TriSlot &Q = slots[w][qq];
+                    const float *st = cr + 3 * slot;
+                    const float *en = cr + 3 * (slot == 2 ? 0 : slot + 1);
+                    float elo[3], ehi[3];
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        elo[d] = fsub(fminf(st[d], en[d]), A.pad);
+                        ehi[d] = fadd(fmaxf(st[d], en[d]), A.pad);
+                    }
+                    e_ok = box_overlap(elo, ehi, Q.clo, Q.chi);
+                }
+                push(e_ok, tri, qq, 3 + slot);
+            }
+            drain(31);
+        }
+    }
+    drain(0);
+    count_hits(A.frame_hits, hits);
+}
+
+__global__ void __launch_bounds__(32 * BATCH_WARPS, CS_DETECT_MINB)
+k_detect_tri(const CollideArgs A, const GridDesc g, const uint2 *__restrict__ cbe,
+             const float4 *__restrict__ rbox, const float *__restrict__ corners,
+             const float *__restrict__ normals, const int32_t *__restrict__ tris,
+             const uint8_t *__restrict__ tri_own, int64_t nc, int qb, int packed) {
+    __shared__ TriShared S;
+    if (packed)
+        detect_tri<true>(S, blockIdx.x, A, g, cbe, rbox, corners, normals, tris, tri_own, nc, qb);
+    else
+        detect_tri<false>(S, blockIdx.x, A, g, cbe, rbox, corners, normals, tris, tri_own, nc, qb);
+}
+
 // Both passes in ONE launch: blocks [0, blocks_a) take cloth edges (pass A),
 // the rest cloth triangles (pass B) -- no dependency between them, one
 // launch latency instead of two.
-#ifndef CS_DETECT_MINB
-#define CS_DETECT_MINB 8  // <= 64 registers, 32 resident warps per SM (strided queries: C3 frame -3%)
-#endif
 __global__ void __launch_bounds__(32 * BATCH_WARPS, CS_DETECT_MINB)
 k_detect_batch(const CollideArgs A, const GridDesc g, const uint2 *__restrict__ cbe,
                const float4 *__restrict__ rbox, const float *__restrict__ corners,
@@ -1107,12 +1389,19 @@ k_detect_batch(const CollideArgs A, const GridDesc g, const uint2 *__restrict__ 
                int qb_a, int64_t blocks_a, const int32_t *__restrict__ tris, int64_t nc, int qb_b,
                int packed) {
     __shared__ BatchShared S;
-    if ((int64_t)blockIdx.x < blocks_a)
-        detect_batch<0>(S, blockIdx.x, A, g, cbe, rbox, corners, normals, edges, ne, qb_a,
-                        packed != 0);
-    else
-        detect_batch<1>(S, blockIdx.x - blocks_a, A, g, cbe, rbox, corners, normals, tris, nc,
-                        qb_b, packed != 0);
+    if ((int64_t)blockIdx.x < blocks_a) {
+        if (packed)
+            detect_batch<0, true>(S, blockIdx.x, A, g, cbe, rbox, corners, normals, edges, ne, qb_a);
+        else
+            detect_batch<0, false>(S, blockIdx.x, A, g, cbe, rbox, corners, normals, edges, ne, qb_a);
+    } else {
+        if (packed)
+            detect_batch<1, true>(S, blockIdx.x - blocks_a, A, g, cbe, rbox, corners, normals, tris,
+                                  nc, qb_b);
+        else
+            detect_batch<1, false>(S, blockIdx.x - blocks_a, A, g, cbe, rbox, corners, normals, tris,
+                                   nc, qb_b);
+    }
 }
 
 __global__ void k_tri_boxes(int64_t nt, const float *__restrict__ corners, float *__restrict__ box) {
@@ -1133,7 +1422,17 @@ void launch_tri_boxes(int64_t nt, const float *corners, float *box, cudaStream_t
 void launch_detect(const CollideArgs &A, const BroadPhase &bp, const float *corners,
                    const float *normals, const int32_t *edges, int64_t ne, const int32_t *tris,
                    int64_t nc, cudaStream_t st) {
-    if (bp.warp_per_query == 2) {
+    if (bp.warp_per_query == 3 && bp.tri_own) {
+        int qb = 32;
+        while (qb > 1 && nc / qb < (int64_t)148 * CS_DETECT_WPSM) qb >>= 1;
+        const int64_t blocks = nc > 0 ? nblk((nc + qb - 1) / qb, BATCH_WARPS) : 0;
+        if (blocks > 0)
+            k_detect_tri<<<(unsigned)blocks, 32 * BATCH_WARPS, 0, st>>>(
+                A, bp.grid, bp.cell_be, bp.ref_box, corners, normals, tris, bp.tri_own, nc, qb,
+                bp.packed_cells ? 1 : 0);
+        return;
+    }
+    if (bp.warp_per_query >= 2) {
         // queries per warp: the largest power of two <= 32 that still leaves
         // >= CS_DETECT_WPSM warps per SM (148 SMs).  With contiguous batches
         // the frame's time was the tail of the warps whose queries sat in the

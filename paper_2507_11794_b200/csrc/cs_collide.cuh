@@ -57,8 +57,12 @@ struct BroadPhase {
     uint2 *cell_be = nullptr;
     float4 *ref_box = nullptr;
     bool packed_cells = false;       // every grid axis <= 1024 cells (10-bit packing)
-    int warp_per_query = 2;          // narrow phase: 32-query batches per warp (2),
-                                     // warp per query (1) or thread per query (0)
+    int warp_per_query = 3;          // narrow phase: one fused candidate enumeration per
+                                     // cloth triangle for both passes (3, default),
+                                     // 32-query batches per warp and pass (2), warp per
+                                     // query (1) or thread per query (0)
+    uint8_t *tri_own = nullptr;      // mode 3: per cloth triangle, the unique edges it owns
+                                     // (bit k: nodes k, k+1 mod 3; each edge owned once)
 };
 
 struct CollideArgs {

@@ -255,7 +255,7 @@ class Engine:
     def __init__(self, mesh, obstacle=None, params=None, device=None,
                  pair_budget: int = DEFAULT_PAIR_BUDGET, *, precision: str = "fast",
                  graph: bool = True, stream=None, cell_size: float | None = None,
-                 force_csr: bool = False, kernel: str = "pair", narrow: str = "batch",
+                 force_csr: bool = False, kernel: str = "pair", narrow: str = "tri",
                  normals: str = "auto", seam: str = "kernel"):
         if precision not in PRECISIONS:
             raise ValueError(f"precision must be one of {PRECISIONS}")
@@ -343,13 +343,16 @@ class Engine:
             raise ValueError("normals must be 'auto', 'fused' (inside the next frame's step "
                              "kernel) or 'split' (stand-alone kernel after each step)")
         flags |= {"auto": 0, "split": N.FLAG_SPLIT_NORMALS, "fused": N.FLAG_FUSE_NORMALS}[normals]
-        if narrow not in ("batch", "warp", "thread"):
-            raise ValueError("narrow must be 'batch' (32 queries per warp, default), 'warp' "
-                             "(warp per query) or 'thread' (thread per query)")
+        if narrow not in ("tri", "batch", "warp", "thread"):
+            raise ValueError("narrow must be 'tri' (one fused candidate enumeration per cloth "
+                             "triangle for both passes, default), 'batch' (batched queries per "
+                             "pass), 'warp' (warp per query) or 'thread' (thread per query)")
         if narrow == "thread":
             flags |= N.FLAG_THREAD_NARROW
         elif narrow == "warp":
             flags |= N.FLAG_WARP_NARROW
+        elif narrow == "batch":
+            flags |= N.FLAG_SPLIT_NARROW
         if kernel == "pair":
             flags |= N.FLAG_PAIRED
         if seam not in ("kernel", "stream"):

@@ -142,7 +142,7 @@ def test_grid_kernels_agree_with_csr(shape):
                 np.testing.assert_allclose(e.read_normals(), ref.read_normals(), atol=1e-5)
 
 
-@pytest.mark.parametrize("narrow", ["batch", "warp", "thread"])
+@pytest.mark.parametrize("narrow", ["tri", "batch", "warp", "thread"])
 @pytest.mark.parametrize("cell", [None, 0.02, 0.003])
 def test_narrow_phase_mappings_and_cell_sizes_are_bit_identical(narrow, cell):
     """The hit set may not depend on how candidates are found."""
@@ -203,7 +203,7 @@ def test_graph_replay_equals_eager_launches():
     assert a.stats()["hit_counter"] == b.stats()["hit_counter"] > 0
 
 
-@pytest.mark.parametrize("narrow", ["batch", "warp"])
+@pytest.mark.parametrize("narrow", ["tri", "batch", "warp"])
 def test_fixed_mode_collision_matches_oracle_on_100k_sphere_state(narrow):
     """One collision frame of C4 (64x64 vs the 99,904-triangle sphere) from a
     draped, perturbed state: accumulators, counts and hits bit-identical to
@@ -279,25 +279,26 @@ def test_c5_fast_mode_against_the_solver_exact_fp64_engine():
 
 
 def test_batched_narrow_phase_equals_warp_per_query_at_full_c3_size():
-    """C3 (316^2 cloth draping onto the 99,904-triangle sphere): the batched
-    narrow phase (default) and the independent warp-per-query mapping find
-    the same contacts every frame -- positions bit-identical and equal hit
-    counts after 250 frames, and the same (node, triangle) contact multiset
-    in the last frame."""
+    """C3 (316^2 cloth draping onto the 99,904-triangle sphere): the fused
+    per-triangle narrow phase (default), the per-pass batched one and the
+    independent warp-per-query mapping find the same contacts every frame --
+    positions bit-identical and equal hit counts after 250 frames, and the
+    same (node, triangle) contact multiset in the last frame."""
     sc = P.baseline_scene("C3")
     engs = [P.Engine(sc.mesh, sc.obstacle, sc.params, pair_budget=10**13, narrow=nw)
-            for nw in ("batch", "warp")]
+            for nw in ("tri", "batch", "warp")]
     for e in engs:
         e.step_frames(249)
         e.enable_contact_log()
         e.step()
-    a, b = engs
-    assert a.stats()["hit_counter"] == b.stats()["hit_counter"] > 0
-    np.testing.assert_array_equal(a.read_positions(), b.read_positions())
-    ca, cb = a.read_contacts(), b.read_contacts()
-    assert len(ca) > 1000
+    a = engs[0]
     key = lambda c: c[np.lexsort((c[:, 1], c[:, 0]))]  # noqa: E731 (multiset order)
-    np.testing.assert_array_equal(key(ca), key(cb))
+    ca = a.read_contacts()
+    assert len(ca) > 1000
+    for b in engs[1:]:
+        assert a.stats()["hit_counter"] == b.stats()["hit_counter"] > 0
+        np.testing.assert_array_equal(a.read_positions(), b.read_positions())
+        np.testing.assert_array_equal(key(ca), key(b.read_contacts()))
 
 
 @pytest.mark.parametrize("n", [120, 200])
@@ -312,15 +313,16 @@ def test_strided_batches_of_every_size_equal_warp_per_query(n):
     sc = build_scene(ScenarioConfig("drop", (n, n), obstacle="uvsphere:224x224", dt=0.002,
                                     stiffness=k, damping=c))
     engs = [P.Engine(sc.mesh, sc.obstacle, sc.params, pair_budget=10**13, narrow=nw)
-            for nw in ("batch", "warp")]
+            for nw in ("tri", "batch", "warp")]
     for e in engs:
         e.step_frames(249)
         e.enable_contact_log()
         e.step()
-    a, b = engs
-    assert a.stats()["hit_counter"] == b.stats()["hit_counter"] > 0
-    np.testing.assert_array_equal(a.read_positions(), b.read_positions())
-    ca, cb = a.read_contacts(), b.read_contacts()
-    assert len(ca) > 100
+    a = engs[0]
     key = lambda c: c[np.lexsort((c[:, 1], c[:, 0]))]  # noqa: E731 (multiset order)
-    np.testing.assert_array_equal(key(ca), key(cb))
+    ca = a.read_contacts()
+    assert len(ca) > 100
+    for b in engs[1:]:
+        assert a.stats()["hit_counter"] == b.stats()["hit_counter"] > 0
+        np.testing.assert_array_equal(a.read_positions(), b.read_positions())
+        np.testing.assert_array_equal(key(ca), key(b.read_contacts()))
