@@ -989,7 +989,10 @@ __device__ __forceinline__ void detect_batch(BatchShared &S, int64_t blk, const 
     int qn = 0;  // queued items (warp-uniform)
     auto drain = [&](int keep) {  // run the predicate on full warps of queued items
         while (qn > keep) {
-            const int take = qn - keep < 32 ? qn - keep : 32;
+            // a FULL warp of items while more than `keep` wait (the excess
+            // alone would run the predicate on a few lanes: ncu saw 5-17
+            // active lanes per predicate instruction)
+            const int take = qn < 32 ? qn : 32;
             __syncwarp();
             if (lane < take) {
                 const int k = qn - take + lane;
@@ -1240,7 +1243,10 @@ __device__ __forceinline__ void detect_tri(TriShared &S, int64_t blk, const Coll
     int qn = 0;  // queued items (warp-uniform)
     auto drain = [&](int keep) {  // run the predicate on full warps of queued items
         while (qn > keep) {
-            const int take = qn - keep < 32 ? qn - keep : 32;
+            // a FULL warp of items while more than `keep` wait (the excess
+            // alone would run the predicate on a few lanes: ncu saw 5-17
+            // active lanes per predicate instruction)
+            const int take = qn < 32 ? qn : 32;
             __syncwarp();
             if (lane < take) {
                 const int k = qn - take + lane;
