@@ -251,6 +251,33 @@ __global__ void k_cell_ranges(const uint32_t *__restrict__ keys, int64_t n,
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
 void launch_tri_boxes(int64_t nt, const float *corners, float *box, cudaStream_t st);
+void launch_edge_boxes(int64_t nt, const float *corners, float4 *box, cudaStream_t st);
+// per obstacle triangle, its 3 edges' boxes padded by BOX_PAD (kernels.py:55-59:
+// lo = min(st, en) - pad, hi = max(st, en) + pad, f32, pad fixed at 1e-5 as
+// CollideArgs::pad), 18 floats in 5 float4 (the fused narrow phase's pass B)
+__global__ void k_edge_boxes(int64_t nt, const float *__restrict__ corners,
+                             float4 *__restrict__ box, float pad) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    const float *c = corners + 9 * t;
+    float f[20];
+#pragma unroll
+    for (int slot = 0; slot < 3; ++slot) {
+        const float *st = c + 3 * slot;
+        const float *en = c + 3 * (slot == 2 ? 0 : slot + 1);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            f[6 * slot + d] = __fsub_rn(fminf(st[d], en[d]), pad);
+            f[6 * slot + 3 + d] = __fadd_rn(fmaxf(st[d], en[d]), pad);
+        }
+    }
+    f[18] = f[19] = 0.f;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) box[5 * t + q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+}
+void launch_edge_boxes(int64_t nt, const float *corners, float4 *box, cudaStream_t st) {
+    if (nt > 0) k_edge_boxes<<<nblk(nt, 256), 256, 0, st>>>(nt, corners, box, 1e-5f);
+}
 
 __global__ void k_pack_cells(int64_t n, const uint32_t *__restrict__ beg,
                              const uint32_t *__restrict__ end, uint2 *__restrict__ be) {
@@ -316,6 +343,7 @@ int build_broadphase(BroadPhase &bp, const float *d_corners, int64_t nt, const f
     g.inv_cell = 1.0f / cs_;
     g.cell = cs_;
     bp.num_cells = (int64_t)dims[0] * dims[1] * dims[2];
+    bp.num_tris = nt;
 
     uint32_t *counts, *offsets;
     cudaMalloc(&counts, (nt + 1) * sizeof(uint32_t));
@@ -350,6 +378,8 @@ int build_broadphase(BroadPhase &bp, const float *d_corners, int64_t nt, const f
     cudaFree(tk);
     cudaMalloc(&bp.tri_box, 6 * (nt > 0 ? nt : 1) * sizeof(float));
     launch_tri_boxes(nt, d_corners, bp.tri_box, st);
+    cudaMalloc(&bp.edge_box, 5 * (nt > 0 ? nt : 1) * sizeof(float4));
+    launch_edge_boxes(nt, d_corners, bp.edge_box, st);
     cudaMalloc(&bp.cell_be, bp.num_cells * sizeof(uint2));
     cudaMalloc(&bp.ref_box, 2 * (total + 1) * sizeof(float4));
     k_pack_cells<<<nblk(bp.num_cells, 256), 256, 0, st>>>(bp.num_cells, bp.cell_begin, bp.cell_end,
@@ -363,6 +393,7 @@ int build_broadphase(BroadPhase &bp, const float *d_corners, int64_t nt, const f
 
 void free_broadphase(BroadPhase &bp) {
     cudaFree(bp.tri_own);
+    cudaFree(bp.edge_box);
     cudaFree(bp.cell_be);
     cudaFree(bp.ref_box);
     cudaFree(bp.cell_begin);
@@ -1138,8 +1169,10 @@ constexpr int QCAP_T = 224;  // < 32 left + 32 lanes x 6 items
 
 struct TriShared {
     TriSlot slots[BATCH_WARPS][32];
-    uint32_t qtri[BATCH_WARPS][QCAP_T];
-    uint8_t qmeta[BATCH_WARPS][QCAP_T];  // query slot << 3 | kind (0-2: edge k; 3-5: slot)
+    // queued item: obstacle triangle | query slot << 27 | kind << 24 (kind
+    // 0-2: the query's edge k, 3-5: obstacle edge slot) -- launch_detect
+    // keeps obstacles under 2^24 triangles on this path
+    uint32_t qitem[BATCH_WARPS][QCAP_T];
 };
 
 // one item: pass A (kind 0-2, the query's edge `kind`) or pass B (kind 3-5,
@@ -1201,12 +1234,11 @@ __device__ __forceinline__ void detect_tri(TriShared &S, int64_t blk, const Coll
                                            const float *__restrict__ corners,
                                            const float *__restrict__ normals,
                                            const int32_t *__restrict__ tris,
-                                           const uint8_t *__restrict__ tri_own, int64_t nq, int qb) {
+                                           const uint8_t *__restrict__ tri_own,
+                                           const float4 *__restrict__ ebox, int64_t nq, int qb) {
     auto &slots = S.slots;
-    auto &qtri = S.qtri;
-    auto &qmeta = S.qmeta;
+    auto &qitem = S.qitem;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint32_t lt_mask = (1u << lane) - 1u;
     // strided queries (as detect_batch): query = lane * warps + warp
     const int64_t nw = (nq + qb - 1) / qb;
     const int64_t wi = blk * BATCH_WARPS + w;
@@ -1249,22 +1281,28 @@ __device__ __forceinline__ void detect_tri(TriShared &S, int64_t blk, const Coll
             const int take = qn < 32 ? qn : 32;
             __syncwarp();
             if (lane < take) {
-                const int k = qn - take + lane;
-                const uint8_t meta = qmeta[w][k];
-                hits += tri_item(A, slots[w][meta >> 3], qtri[w][k], meta & 7, corners, normals);
+                const uint32_t it = qitem[w][qn - take + lane];
+                hits += tri_item(A, slots[w][it >> 27], it & 0xffffffu, (int)((it >> 24) & 7u),
+                                 corners, normals);
             }
             qn -= take;
             __syncwarp();
         }
     };
-    auto push = [&](bool want, uint32_t tri, int qs, int kind) {
-        const uint32_t m = __ballot_sync(0xffffffffu, want);
-        if (want) {
-            const int k = qn + __popc(m & lt_mask);
-            qtri[w][k] = tri;
-            qmeta[w][k] = (uint8_t)((qs << 3) | kind);
+    // queue every item of this lane's candidate at once: bit k of `items`
+    // = kind k (0-2 pass A edges, 3-5 pass B edge slots); one warp scan
+    // places them
+    auto push6 = [&](uint32_t items, uint32_t tri, int qs) {
+        const uint32_t n = __popc(items);
+        const uint32_t incl = warp_incl_scan(n);
+        int k = qn + (int)(incl - n);
+        const uint32_t head = tri | ((uint32_t)qs << 27);
+        while (items) {
+            const int kind = __ffs(items) - 1;
+            items &= items - 1u;
+            qitem[w][k++] = head | ((uint32_t)kind << 24);
         }
-        qn += __popc(m);
+        qn += (int)__shfl_sync(0xffffffffu, incl, 31);
     };
     const uint32_t cincl = warp_incl_scan(ncell);
     const uint32_t ctotal = __shfl_sync(0xffffffffu, cincl, 31);
@@ -1325,15 +1363,14 @@ __device__ __forceinline__ void detect_tri(TriShared &S, int64_t blk, const Coll
                          g.cell_of(fmaxf(Q.lo[2], tlo[2]), 2) == oz;
                 }
             }
-            // pass A: the query's owned edges whose padded box meets the
-            // obstacle triangle's box (kernels.py:55-78)
+            uint32_t items = 0;
+            if (ok) {
+                const TriSlot &Q = slots[w][qq];
+                // pass A: the query's owned edges whose padded box meets the
+                // obstacle triangle's box (kernels.py:55-78)
 #pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                bool e_ok = ok;
-                if (e_ok) {
-                    const TriSlot &Q = slots[w][qq];
-                    e_ok = (Q.own >> k) & 1u;
-                    if (e_ok) {
+                for (int k = 0; k < 3; ++k) {
+                    if ((Q.own >> k) & 1u) {
                         const int k1 = k == 2 ? 0 : k + 1;
                         float elo[3], ehi[3];
 #pragma unroll
@@ -1341,31 +1378,21 @@ __device__ __forceinline__ void detect_tri(TriShared &S, int64_t blk, const Coll
                             elo[d] = fsub(fminf(Q.v[k][d], Q.v[k1][d]), A.pad);
                             ehi[d] = fadd(fmaxf(Q.v[k][d], Q.v[k1][d]), A.pad);
                         }
-                        e_ok = box_overlap(elo, ehi, tlo, thi);
+                        if (box_overlap(elo, ehi, tlo, thi)) items |= 1u << k;
                     }
                 }
-                push(e_ok, tri, qq, k);
+                // pass B: obstacle edges 3t+slot whose padded box (precomputed,
+                // the same f32 operations) meets the cloth triangle's box
+                const float4 *eb = ebox + 5 * (int64_t)tri;
+                const float4 e0 = eb[0], e1 = eb[1], e2 = eb[2], e3 = eb[3], e4 = eb[4];
+                const float b0lo[3] = {e0.x, e0.y, e0.z}, b0hi[3] = {e0.w, e1.x, e1.y};
+                const float b1lo[3] = {e1.z, e1.w, e2.x}, b1hi[3] = {e2.y, e2.z, e2.w};
+                const float b2lo[3] = {e3.x, e3.y, e3.z}, b2hi[3] = {e3.w, e4.x, e4.y};
+                if (box_overlap(b0lo, b0hi, Q.clo, Q.chi)) items |= 8u;
+                if (box_overlap(b1lo, b1hi, Q.clo, Q.chi)) items |= 16u;
+                if (box_overlap(b2lo, b2hi, Q.clo, Q.chi)) items |= 32u;
             }
-            // pass B: obstacle edges 3t+slot whose padded box meets the cloth
-            // triangle's box
-            const float *cr = corners + 9 * (int64_t)tri;
-#pragma unroll
-            for (int slot = 0; slot < 3; ++slot) {
-                bool e_ok = ok;
-                if (e_ok) {
-                    const TriSlot &Q = slots[w][qq];
-                    const float *st = cr + 3 * slot;
-                    const float *en = cr + 3 * (slot == 2 ? 0 : slot + 1);
-                    float elo[3], ehi[3];
-#pragma unroll
-                    for (int d = 0; d < 3; ++d) {
-                        elo[d] = fsub(fminf(st[d], en[d]), A.pad);
-                        ehi[d] = fadd(fmaxf(st[d], en[d]), A.pad);
-                    }
-                    e_ok = box_overlap(elo, ehi, Q.clo, Q.chi);
-                }
-                push(e_ok, tri, qq, 3 + slot);
-            }
+            push6(items, tri, qq);
             drain(31);
         }
     }
@@ -1377,12 +1404,15 @@ __global__ void __launch_bounds__(32 * BATCH_WARPS, CS_DETECT_MINB)
 k_detect_tri(const CollideArgs A, const GridDesc g, const uint2 *__restrict__ cbe,
              const float4 *__restrict__ rbox, const float *__restrict__ corners,
              const float *__restrict__ normals, const int32_t *__restrict__ tris,
-             const uint8_t *__restrict__ tri_own, int64_t nc, int qb, int packed) {
+             const uint8_t *__restrict__ tri_own, const float4 *__restrict__ ebox, int64_t nc,
+             int qb, int packed) {
     __shared__ TriShared S;
     if (packed)
-        detect_tri<true>(S, blockIdx.x, A, g, cbe, rbox, corners, normals, tris, tri_own, nc, qb);
+        detect_tri<true>(S, blockIdx.x, A, g, cbe, rbox, corners, normals, tris, tri_own, ebox, nc,
+                         qb);
     else
-        detect_tri<false>(S, blockIdx.x, A, g, cbe, rbox, corners, normals, tris, tri_own, nc, qb);
+        detect_tri<false>(S, blockIdx.x, A, g, cbe, rbox, corners, normals, tris, tri_own, ebox,
+                          nc, qb);
 }
 
 // Both passes in ONE launch: blocks [0, blocks_a) take cloth edges (pass A),
@@ -1428,14 +1458,14 @@ void launch_tri_boxes(int64_t nt, const float *corners, float *box, cudaStream_t
 void launch_detect(const CollideArgs &A, const BroadPhase &bp, const float *corners,
                    const float *normals, const int32_t *edges, int64_t ne, const int32_t *tris,
                    int64_t nc, cudaStream_t st) {
-    if (bp.warp_per_query == 3 && bp.tri_own) {
+    if (bp.warp_per_query == 3 && bp.tri_own && bp.num_tris < (1 << 24)) {
         int qb = 32;
         while (qb > 1 && nc / qb < (int64_t)148 * CS_DETECT_WPSM) qb >>= 1;
         const int64_t blocks = nc > 0 ? nblk((nc + qb - 1) / qb, BATCH_WARPS) : 0;
         if (blocks > 0)
             k_detect_tri<<<(unsigned)blocks, 32 * BATCH_WARPS, 0, st>>>(
-                A, bp.grid, bp.cell_be, bp.ref_box, corners, normals, tris, bp.tri_own, nc, qb,
-                bp.packed_cells ? 1 : 0);
+                A, bp.grid, bp.cell_be, bp.ref_box, corners, normals, tris, bp.tri_own, bp.edge_box,
+                nc, qb, bp.packed_cells ? 1 : 0);
         return;
     }
     if (bp.warp_per_query >= 2) {

@@ -46,11 +46,14 @@ struct BroadPhase {
     GridDesc grid{};
     int64_t num_cells = 0;
     int64_t num_refs = 0;
+    int64_t num_tris = 0;            // obstacle triangles
     uint32_t *cell_begin = nullptr;  // per cell: first index into cell_tris
     uint32_t *cell_end = nullptr;
     uint32_t *cell_keys = nullptr;   // sorted (cell key) per reference
     uint32_t *cell_tris = nullptr;   // triangle id per reference
     float *tri_box = nullptr;        // per triangle: lo xyz, hi xyz (kernels.py:62-66)
+    float4 *edge_box = nullptr;      // per triangle: its 3 edges' padded boxes (kernels.py:55-59),
+                                     // lo xyz hi xyz per edge, 18 floats in 5 float4`s
     // batched narrow phase: (begin, end) per cell in one 8-byte word, and per
     // sorted reference its triangle's box with the triangle id in lo.w --
     // one 32-byte load per candidate instead of ctri -> tri_box

@@ -14,7 +14,7 @@ from paper_2507_11794_b200 import _native as N
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C3"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 50
-narrow = os.environ.get("CS_NARROW", "batch")
+narrow = os.environ.get("CS_NARROW", "tri")
 sc = P.baseline_scene(cfg)
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
