@@ -1,4 +1,4 @@
-"""Copy a profile_round.sh bundle from gpurun_out/ into profiles/ (round 1):
+"""Copy a profile_round.sh bundle from gpurun_out/ into profiles/ (ROUND, default r2):
 bench line, launch list, ncu summaries, traffic.json and the SASS of the
 dominant kernels.  Run here after the GPU call.
 
@@ -38,32 +38,38 @@ def raw_bytes(rep):
     return res
 
 
-shutil.copy(os.path.join(G, "bench.json"), os.path.join(P, "r1_bench_c2.json"))
-shutil.copy(os.path.join(G, "launches.csv"), os.path.join(P, "r1_c2_bench_launches.csv"))
-with open(os.path.join(P, "r1_ncu_summary.txt"), "w") as fh:
-    fh.write("# round 1: ncu --set full --clock-control none, one launch per kernel "
+R = os.environ.get("ROUND", "r2")
+shutil.copy(os.path.join(G, "bench.json"), os.path.join(P, f"{R}_bench.json"))
+shutil.copy(os.path.join(G, "launches.csv"), os.path.join(P, f"{R}_bench_launches.csv"))
+with open(os.path.join(P, f"{R}_ncu_summary.txt"), "w") as fh:
+    fh.write(f"# {R}: ncu --set full --clock-control none, one launch per kernel "
              "(cold-cache replays: the kernel's share of the step, not its absolute time)\n")
     fh.write("# C2 frame kernel (k_pair3<1,0>, 640K nodes)\n" + summary(os.path.join(G, "c2_frame.ncu-rep"), 1))
-    fh.write("# C5 fused frame kernel (k_pair3<1,0>, 16.8M nodes)\n" + summary(os.path.join(G, "c5_passes.ncu-rep"), 1))
-    fh.write("# C5 split passes: stand-alone k_pair_normals, force+integrate k_pair3<0,0>\n" + summary(os.path.join(G, "c5_split.ncu-rep"), 2))
-    fh.write("# C3 collision (draped: after 200 frames): batched narrow phase + respond\n" + summary(os.path.join(G, "c3_draped.ncu-rep")))
-t = {"_source": "ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum per launch "
-                "(profiles/r1_ncu_summary.txt): C2 / C5_frame = fused k_pair3<1,0>, "
-                "C5 = k_pair3<0,0> force pass, C5_normals = k_pair_normals"}
+    fh.write("# C5 fused frame kernel (k_pair3<1,0>, 16.8M nodes)\n" + summary(os.path.join(G, "c5_frame.ncu-rep"), 1))
+    fh.write("# C5 split passes: stand-alone k_pair_normals, then force+integrate k_pair3<0,0>\n" + summary(os.path.join(G, "c5_split.ncu-rep"), 2))
+    fh.write("# C3 collision (draped: after 200 frames): fused narrow phase + respond\n" + summary(os.path.join(G, "c3_draped.ncu-rep")))
+t = {"_source": f"ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                f"(profiles/{R}_ncu_summary.txt): C2 / C5_frame = fused k_pair3<1,0>, "
+                "C5 = k_pair3<0,0> force pass, C5_normals = k_pair_normals, C3_detect = the "
+                "fused narrow phase of a draped C3 frame"}
 t["C2"] = raw_bytes(os.path.join(G, "c2_frame.ncu-rep"))[0][1]
-t["C5_frame"] = raw_bytes(os.path.join(G, "c5_passes.ncu-rep"))[0][1]
+t["C5_frame"] = raw_bytes(os.path.join(G, "c5_frame.ncu-rep"))[0][1]
 for name, b in raw_bytes(os.path.join(G, "c5_split.ncu-rep")):
     if "normals" in name:
         t.setdefault("C5_normals", b)
     else:
         t.setdefault("C5", b)
+for name, b in raw_bytes(os.path.join(G, "c3_draped.ncu-rep")):
+    if "detect" in name:
+        t.setdefault("C3_detect", b)
 json.dump(t, open(os.path.join(P, "traffic.json"), "w"), indent=2)
 print(json.dumps(t, indent=1))
 
 lib = os.path.join(ROOT, "paper_2507_11794_b200", "_lib", "libclothsim_b200.so")
 sass = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
-want = {"k_pair3ILb1ELb0": "r1_sass_k_pair3_fused.txt", "k_pair3ILb0ELb0": "r1_sass_k_pair3_force.txt",
-        "k_detect_batch": "r1_sass_k_detect_batch.txt"}
+want = {"k_pair3ILb1ELb0ELb0": f"{R}_sass_k_pair3_fused.txt",
+        "k_pair3ILb0ELb0ELb0": f"{R}_sass_k_pair3_force.txt",
+        "k_detect_tri": f"{R}_sass_k_detect_tri.txt"}
 for part in sass.split("Function : ")[1:]:
     name = part.split("\n", 1)[0]
     for k, f in want.items():
