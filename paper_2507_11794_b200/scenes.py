@@ -87,6 +87,7 @@ class Scene:
     external_accel: np.ndarray | None = None
     sphere_center: np.ndarray | None = None
     sphere_radius: float | None = None
+    snapshot_axis: str = "y"  # scenes.py:157 (hanging "z", drop / pull "x")
 
 
 def parse_obstacle_spec(spec: str):
@@ -165,14 +166,14 @@ def build_scene(config: ScenarioConfig) -> Scene:
         mesh = generate_cloth_grid(nx, ny, CLOTH_SIZE, CLOTH_SIZE,
                                    total_mass=NODE_MASS * nx * ny, pinned_rows="first")
         mesh.positions = _rotate_xz_to_xy(mesh.positions)
-        return Scene("hanging", mesh, _params(config))
+        return Scene("hanging", mesh, _params(config), snapshot_axis="z")
     mesh, params, obstacle, center, radius = _cloth_over_obstacle(config)
     if config.scene == "drop":
-        return Scene("drop", mesh, params, obstacle, None, center, radius)
+        return Scene("drop", mesh, params, obstacle, None, center, radius, snapshot_axis="x")
     nx, ny = config.grid
     accel = np.zeros((mesh.num_nodes, 3))
     accel[[mesh.node_index(nx - 1, j) for j in range(ny)], 0] = config.pull_accel
-    return Scene("pull", mesh, params, obstacle, accel, center, radius)
+    return Scene("pull", mesh, params, obstacle, accel, center, radius, snapshot_axis="x")
 
 
 def corner_pinned_cloth(n: int, dt: float = CONTACT_DT) -> Scene:
