@@ -94,6 +94,9 @@ struct cs_engine {
     bool fuse_normals() const {
         if (!(grid && strip)) return false;
         if (flags & CS_FLAG_SPLIT_NORMALS) return false;
+        // the reference-exact paired kernel integrates only; its frame runs
+        // the exact normals kernel after it
+        if (fixed && (flags & CS_FLAG_PAIRED)) return false;
         return true;
     }
     bool normals_stale = false; // normals buffer holds the previous frame's (fused)
@@ -522,7 +525,7 @@ static int seam_check(cs_engine *h) {
 static int banded_frame(cs_engine *h) {
     const bool fuse = h->fuse_normals();
     const bool packed = (h->flags & CS_FLAG_PAIRED) != 0;
-    const bool fused_push = !h->fixed && packed;  // k_pair3 stores into the peers itself
+    const bool fused_push = packed;  // k_pair3 (fast or exact) stores into the peers itself
     for (int s = 0; s < h->substeps; ++s) {
         if (int r = halo_wait(h)) return r;
         if (s == 0 && !fuse) pass_normals(h);  // the frame's starting state, halo complete
@@ -661,6 +664,9 @@ static int build(cs_engine *h, const cs_desc *d) {
     sp.inv_mass = im_free;
     sp.scale_f = (float)d->fixed_point_scale;
     sp.scale_d = (double)d->fixed_point_scale;
+    sp.inv_scale_pow2 = 0.f;
+    if (d->fixed_point_scale > 0 && (d->fixed_point_scale & (d->fixed_point_scale - 1)) == 0)
+        sp.inv_scale_pow2 = (float)(1.0 / (double)d->fixed_point_scale);
     sp.explicit_euler = (d->flags & CS_FLAG_EXPLICIT_EULER) ? 1 : 0;
     sp.row_lo = 0;
     sp.row_hi = sp.ny;

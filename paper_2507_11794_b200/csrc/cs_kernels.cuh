@@ -190,7 +190,7 @@ void launch_strip_step(const StepParams &p, bool fixed, bool normals, const floa
                        cudaStream_t st, bool packed = false, const HaloDst *halo = nullptr);
 void launch_pair3_step(const StepParams &p, bool normals, const float *src, float *dst,
                        const uint32_t *pinbits, const float *ext, float *nrm, cudaStream_t st,
-                       const HaloDst *halo = nullptr);
+                       const HaloDst *halo = nullptr, bool exact = false);
 // copy rows [r0, r1) of the six planes of `src` to the (pre-shifted) planes `to`
 void launch_push_rows(const float *src, int64_t plane, int pitch, int r0, int r1,
                       float *const to[6], cudaStream_t st);

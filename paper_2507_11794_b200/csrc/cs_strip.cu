@@ -285,8 +285,8 @@ k_strip_step(const StepParams p, const float *__restrict__ src, float *__restric
 void launch_strip_step(const StepParams &p, bool fixed, bool normals, const float *src,
                        float *dst, const uint32_t *pinbits, const float *ext, float *nrm,
                        cudaStream_t st, bool packed, const HaloDst *halo) {
-    if (!fixed && packed) {  // paired-column f32x2 kernel: cs_pair3.cu
-        launch_pair3_step(p, normals, src, dst, pinbits, ext, nrm, st, halo);
+    if (packed) {  // paired-column f32x2 kernel (fast or reference-exact): cs_pair3.cu
+        launch_pair3_step(p, normals && !fixed, src, dst, pinbits, ext, nrm, st, halo, fixed);
         return;
     }
     // Tall strips amortise the 2-row vertical halo; small grids get shorter
