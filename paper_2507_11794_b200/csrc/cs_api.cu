@@ -391,8 +391,11 @@ static void pass_normals(cs_engine *h) {
     if (h->fp64) {
         launch_csr_normals_f64(h->N, h->plane, h->nc, (const double *)h->state[h->cur], h->tris_g,
                                (double *)h->face, h->inc_off, h->inc_tri, (double *)h->normals, h->st);
-    } else if (h->grid && !h->fixed && h->strip && (h->flags & CS_FLAG_PAIRED)) {
-        launch_pair_normals(h->sp, (const float *)h->state[h->cur], (float *)h->normals, h->st);
+    } else if (h->grid && h->strip && (h->flags & CS_FLAG_PAIRED)) {
+        if (h->fixed)
+            launch_pair_normals_exact(h->sp, (const float *)h->state[h->cur], (float *)h->normals, h->st);
+        else
+            launch_pair_normals(h->sp, (const float *)h->state[h->cur], (float *)h->normals, h->st);
     } else if (h->grid) {
         launch_grid_normals(h->sp, h->fixed, (const float *)h->state[h->cur], (float *)h->normals, h->st);
     } else {

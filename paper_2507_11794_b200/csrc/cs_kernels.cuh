@@ -195,6 +195,9 @@ void launch_pair3_step(const StepParams &p, bool normals, const float *src, floa
 void launch_push_rows(const float *src, int64_t plane, int pitch, int r0, int r1,
                       float *const to[6], cudaStream_t st);
 void launch_pair_normals(const StepParams &p, const float *state, float *nrm, cudaStream_t st);
+// reference-exact normals (kernels.py:314-339) in the same paired strip layout
+void launch_pair_normals_exact(const StepParams &p, const float *state, float *nrm,
+                               cudaStream_t st);
 int pair3_rows(const StepParams &p);
 void launch_pair3_forces(const StepParams &p, const float *src, const uint32_t *pinbits,
                          int32_t *forces, cudaStream_t st);

@@ -29,4 +29,15 @@ for prec in ("fast", "fixed", "fp64"):
     ms = a.elapsed_time(b) / k
     print(f"{cfg} {prec:5s}: {ms * 1e3:8.1f} us/frame  {1000 / ms:9.0f} steps/s  "
           f"({eng.kernels_per_frame} kernels/frame)", flush=True)
+    # the passes alone (force + integrate, normals)
+    from paper_2507_11794_b200 import _native as N
+    for name, pid in (("force+integrate", N.PASS_FORCE_INTEGRATE), ("normals", N.PASS_NORMALS)):
+        N.check(eng._lib.cs_run_pass(eng._handle, pid))
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(k):
+            N.check(eng._lib.cs_run_pass(eng._handle, pid))
+        b.record(stream)
+        torch.cuda.synchronize()
+        print(f"    {name:16s} {a.elapsed_time(b) / k * 1e3:8.1f} us", flush=True)
     eng.close()
