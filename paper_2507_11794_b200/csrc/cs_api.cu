@@ -94,8 +94,9 @@ struct cs_engine {
     bool fuse_normals() const {
         if (!(grid && strip)) return false;
         if (flags & CS_FLAG_SPLIT_NORMALS) return false;
-        // the reference-exact paired kernel integrates only; its frame runs
-        // the exact normals kernel after it
+        // the reference-exact paired kernel integrates only: its frame runs
+        // the exact normals kernel after it (fused into the step kernel the
+        // exact normals made the C2 frame slower, 59.8 vs 55.9 us)
         if (fixed && (flags & CS_FLAG_PAIRED)) return false;
         return true;
     }

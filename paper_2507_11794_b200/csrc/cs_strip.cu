@@ -286,7 +286,7 @@ void launch_strip_step(const StepParams &p, bool fixed, bool normals, const floa
                        float *dst, const uint32_t *pinbits, const float *ext, float *nrm,
                        cudaStream_t st, bool packed, const HaloDst *halo) {
     if (packed) {  // paired-column f32x2 kernel (fast or reference-exact): cs_pair3.cu
-        launch_pair3_step(p, normals && !fixed, src, dst, pinbits, ext, nrm, st, halo, fixed);
+        launch_pair3_step(p, normals, src, dst, pinbits, ext, nrm, st, halo, fixed);
         return;
     }
     // Tall strips amortise the 2-row vertical halo; small grids get shorter

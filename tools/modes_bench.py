@@ -15,9 +15,9 @@ k = int(sys.argv[2]) if len(sys.argv) > 2 else 50
 sc = P.baseline_scene(cfg)
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
-for prec in ("fast", "fixed", "fp64"):
+for prec in os.environ.get("CS_MODES", "fast,fixed,fp64").split(","):
     eng = P.Engine(sc.mesh, sc.obstacle, sc.params, pair_budget=10**13, precision=prec,
-                   stream=stream.cuda_stream)
+                   stream=stream.cuda_stream, normals=os.environ.get("CS_NORMALS", "auto"))
     eng.step_frames(5 if sc.obstacle is None else 200)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
