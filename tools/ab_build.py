@@ -13,9 +13,4 @@ from paper_2507_11794_b200 import build as B
 
 name, flags = sys.argv[1], sys.argv[2:]
 out = os.path.join(B.LIB_DIR, f"var_{name}.so")
-cmd = [B.nvcc_path(), "-O3", "-std=c++17", *B.ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
-       "-I", B.INCLUDE, *flags, "-o", out] + [os.path.join(B.CSRC, s) for s in B.SOURCES]
-r = subprocess.run(cmd, capture_output=True, text=True)
-if r.returncode:
-    sys.exit(r.stderr)
-print(out)
+print(B.build(force=True, extra_flags=flags, out=out))
