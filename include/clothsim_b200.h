@@ -184,6 +184,46 @@ typedef struct cs_stats {
 #define CS_PASS_NORMALS 3
 
 int cs_create(const cs_desc *desc, cs_engine **out);
+
+/* ---- generate_cloth_grid on the device (mesh.py:223-317) ----
+   A stencil engine straight from the grid's parameters: positions
+   (np.linspace in float64, then the scene's orientation), uniform masses
+   (total_mass / (nx*ny)), whole pinned rows and the six spring families'
+   rest lengths are generated by kernels -- no per-node or per-spring host
+   array, so a 4096^2 cloth builds in a fraction of a second (the reference's
+   Python loops take minutes).  rows [row_lo, row_hi) of the global nx x ny
+   grid form the local sheet (a row band; 0, ny for the whole cloth).
+   orientation: 0 = the generation plane (x, 0, z); 1 = the hanging scene's
+   (x, -z, 0) (scenes.py _rotate_xz_to_xy).  Fails with CS_E_INVALID when a
+   spring family's rest lengths round to two float32 values (SURVEY.md
+   finding 4) -- build from the mesh then.  Fast or fixed arithmetic only. */
+typedef struct cs_grid_desc {
+    int32_t abi_version;       /* = CS_ABI_VERSION */
+    uint32_t flags;            /* cs_desc flags (CS_FLAG_FIXED_POINT, ...) */
+    int32_t nx, ny;            /* the whole grid */
+    int32_t row_lo, row_hi;    /* local rows */
+    double width, height, total_mass;
+    int32_t orientation;
+    int32_t num_pinned_rows;   /* global row indices (mesh.py:320-331) */
+    const int32_t *pinned_rows;
+    double dt;                 /* per substep */
+    double gravity[3];
+    double stiffness[3];
+    double damping;
+    float epsilon_mt;
+    float response_margin;
+    int32_t fixed_point_scale;
+    int32_t substeps;
+    void *stream;
+} cs_grid_desc;
+int cs_create_grid(const cs_grid_desc *desc, cs_engine **out);
+/* generate_cloth_grid's arrays of the local sheet (local node indices,
+   nx x (row_hi - row_lo) nodes, the reference's orders) into DEVICE memory:
+   springs (S,2) i32, kinds (S,) i32, rest (S,) f64, triangles (C,3) i32,
+   positions (N,3) f64 in the generation plane; any output may be NULL. */
+int cs_grid_topology(int32_t nx, int32_t ny, int32_t row_lo, int32_t row_hi, double width,
+                     double height, int32_t *springs, int32_t *kinds, double *rest,
+                     int32_t *tris, double *positions, void *stream);
 int cs_destroy(cs_engine *h);
 /* Advance `frames` whole frames (asynchronous on the engine's stream). */
 int cs_step(cs_engine *h, int32_t frames);

@@ -88,6 +88,32 @@ class CsDesc(ctypes.Structure):
     ]
 
 
+class CsGridDesc(ctypes.Structure):
+    _fields_ = [
+        ("abi_version", ctypes.c_int32),
+        ("flags", ctypes.c_uint32),
+        ("nx", ctypes.c_int32),
+        ("ny", ctypes.c_int32),
+        ("row_lo", ctypes.c_int32),
+        ("row_hi", ctypes.c_int32),
+        ("width", ctypes.c_double),
+        ("height", ctypes.c_double),
+        ("total_mass", ctypes.c_double),
+        ("orientation", ctypes.c_int32),
+        ("num_pinned_rows", ctypes.c_int32),
+        ("pinned_rows", _P),
+        ("dt", ctypes.c_double),
+        ("gravity", ctypes.c_double * 3),
+        ("stiffness", ctypes.c_double * 3),
+        ("damping", ctypes.c_double),
+        ("epsilon_mt", ctypes.c_float),
+        ("response_margin", ctypes.c_float),
+        ("fixed_point_scale", ctypes.c_int32),
+        ("substeps", ctypes.c_int32),
+        ("stream", _P),
+    ]
+
+
 class CsStats(ctypes.Structure):
     _fields_ = [("hits", _I64), ("responded", _I64), ("frames", _I64), ("hit_counter", _I64)]
 
@@ -106,6 +132,9 @@ class CsHaloPeer(ctypes.Structure):
 # every symbol include/clothsim_b200.h declares, with its signature
 SIGNATURES = {
     "cs_create": (_I32, [ctypes.POINTER(CsDesc), ctypes.POINTER(_P)]),
+    "cs_create_grid": (_I32, [ctypes.POINTER(CsGridDesc), ctypes.POINTER(_P)]),
+    "cs_grid_topology": (_I32, [_I32, _I32, _I32, _I32, ctypes.c_double, ctypes.c_double, _P, _P,
+                                _P, _P, _P, _P]),
     "cs_destroy": (_I32, [_P]),
     "cs_step": (_I32, [_P, _I32]),
     "cs_run_pass": (_I32, [_P, _I32]),

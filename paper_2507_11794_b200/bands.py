@@ -158,21 +158,32 @@ class BandedEngine:
         self._opened = []
         self.plan = HaloPlan(ny, world, rank)
         self.nx, self.ny = nx, ny
-        if mesh is not None:
-            stencil = _grid_stencil_rest(mesh)
-            if stencil is None or (stencil[0], stencil[1]) != (nx, ny):
-                raise ValueError("row bands need an nx x ny grid mesh with uniform spring families")
-            band = band_of_mesh(mesh, nx, ny, stencil[2], self.plan.l0, self.plan.l1)
+        if mesh is None and obstacle is None and precision in ("fast", "fixed"):
+            # the hanging cloth's band generated on the device (cs_create_grid):
+            # no per-node or per-spring host array, even at 4096^2
+            self.engine = Engine.from_grid(nx, ny, params, width=width, height=height,
+                                           total_mass=node_mass * nx * ny,
+                                           pinned_rows=pinned_rows, orientation="hanging",
+                                           row_lo=self.plan.l0, row_hi=self.plan.l1,
+                                           stream=stream, precision=precision, **engine_kw)
+            self.mesh = self.engine.mesh
         else:
-            band = grid_band(nx, ny, self.plan.l0, self.plan.l1, width, height,
-                             total_mass=node_mass * nx * ny, pinned_rows=pinned_rows)
-            rot = np.zeros_like(band.positions)  # scenes._rotate_xz_to_xy
-            rot[:, 0] = band.positions[:, 0]
-            rot[:, 1] = -band.positions[:, 2]
-            band.positions = rot
-        self.mesh = band
-        self.engine = Engine(band, obstacle, params=params, stream=stream, precision=precision,
-                             **engine_kw)
+            if mesh is not None:
+                stencil = _grid_stencil_rest(mesh)
+                if stencil is None or (stencil[0], stencil[1]) != (nx, ny):
+                    raise ValueError("row bands need an nx x ny grid mesh with uniform spring "
+                                     "families")
+                band = band_of_mesh(mesh, nx, ny, stencil[2], self.plan.l0, self.plan.l1)
+            else:
+                band = grid_band(nx, ny, self.plan.l0, self.plan.l1, width, height,
+                                 total_mass=node_mass * nx * ny, pinned_rows=pinned_rows)
+                rot = np.zeros_like(band.positions)  # scenes._rotate_xz_to_xy
+                rot[:, 0] = band.positions[:, 0]
+                rot[:, 1] = -band.positions[:, 2]
+                band.positions = rot
+            self.mesh = band
+            self.engine = Engine(band, obstacle, params=params, stream=stream,
+                                 precision=precision, **engine_kw)
         self.group = group
         self.local_rows = self.plan.l1 - self.plan.l0
 

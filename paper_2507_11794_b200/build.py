@@ -21,7 +21,7 @@ LIB_DIR = os.path.join(HERE, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "libclothsim_b200.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 SOURCES = ["cs_api.cu", "cs_grid.cu", "cs_strip.cu", "cs_pair3.cu", "cs_csr.cu", "cs_collide.cu",
-           "cs_collide64.cu", "cs_snapshot.cu"]
+           "cs_collide64.cu", "cs_snapshot.cu", "cs_gridgen.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -26,6 +26,27 @@
 
 using namespace cs;
 
+namespace cs {  // cs_gridgen.cu
+cudaError_t grid_positions(int nx, int ny, int row0, int rows, double width, double height,
+                           int orient, int64_t pitch, int64_t plane, float *state, double *pos64,
+                           cudaStream_t st);
+cudaError_t grid_rest6(int nx, int ny, int row0, int rows, double width, double height,
+                       float rest6[6], bool *uniform, cudaStream_t st);
+cudaError_t grid_topology(int nx, int ny, int row0, int rows, double width, double height,
+                          int32_t *springs, int32_t *kinds, double *rest, int32_t *tris,
+                          double *pos64, cudaStream_t st);
+}  // namespace cs
+
+// a grid engine generated on the device (cs_create_grid): the global grid,
+// the local rows, the uniform inverse mass and the pinned global rows
+struct GridGen {
+    int nx, ny, row0;
+    double width, height;
+    int orient;
+    float inv_mass;
+    std::vector<int> pinned_rows;
+};
+
 static thread_local std::string g_err;
 
 static int fail(int code, const std::string &msg) {
@@ -593,7 +614,15 @@ static void flush_normals(cs_engine *h) {
 extern "C" int cs_abi_version(void) { return CS_ABI_VERSION; }
 extern "C" const char *cs_last_error(void) { return g_err.c_str(); }
 
-static int build(cs_engine *h, const cs_desc *d) {
+__global__ void k_fill_inv_mass(int64_t rows, int64_t nx, int64_t pitch, float im,
+                                const uint32_t *__restrict__ pinbits, float *__restrict__ out) {
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= rows * nx) return;
+    const int64_t g = (v / nx) * pitch + (v % nx);
+    out[g] = ((pinbits[g >> 5] >> (g & 31)) & 1u) ? 0.f : im;
+}
+
+static int build(cs_engine *h, const cs_desc *d, const GridGen *gen = nullptr) {
     const int64_t N = d->num_nodes;
     h->flags = d->flags;
     h->fixed = (d->flags & CS_FLAG_FIXED_POINT) != 0;
@@ -609,9 +638,9 @@ static int build(cs_engine *h, const cs_desc *d) {
         return fail(CS_E_INVALID, "float64 engines need masses64, pinned and spring_rest64");
 
     // uniform inverse mass among free nodes => grid stencil eligible
-    float im_free = 0.f;
+    float im_free = gen ? gen->inv_mass : 0.f;
     bool uniform = true;
-    for (int64_t i = 0; i < N; ++i) {
+    for (int64_t i = 0; !gen && i < N; ++i) {
         const float v = d->inv_mass[i];
         if (v > 0.f) {
             if (im_free == 0.f) im_free = v;
@@ -709,6 +738,9 @@ static int build(cs_engine *h, const cs_desc *d) {
             if (int r = upload_planes<float>(h, d->positions, (float *)h->state[1], 3)) return r;
             k_f32_to_f64<<<nb(3 * P), 256, 0, h->st>>>(3 * P, (const float *)h->state[1], (double *)h->state[0]);
         }
+    } else if (gen) {
+        CK(grid_positions(gen->nx, gen->ny, gen->row0, (int)h->rows, gen->width, gen->height,
+                          gen->orient, h->pitch, P, (float *)h->state[0], nullptr, h->st));
     } else {
         if (int r = upload_planes<float>(h, d->positions, (float *)h->state[0], 3)) return r;
     }
@@ -718,17 +750,35 @@ static int build(cs_engine *h, const cs_desc *d) {
     if (h->grid) {
         const int64_t words = (P + 31) / 32;
         std::vector<uint32_t> bits(words, 0u);
-        for (int64_t n = 0; n < N; ++n)
-            if (!(d->inv_mass[n] > 0.f)) {
-                const int64_t g = h->gidx(n);
-                bits[g >> 5] |= 1u << (g & 31);
+        if (gen) {  // whole pinned rows (mesh.py:260-263)
+            for (int j : gen->pinned_rows) {
+                const int64_t lj = j - gen->row0;
+                if (lj < 0 || lj >= h->rows) continue;
+                for (int64_t i = 0; i < h->nx; ++i) {
+                    const int64_t g = lj * h->pitch + i;
+                    bits[g >> 5] |= 1u << (g & 31);
+                }
             }
+        } else {
+            for (int64_t n = 0; n < N; ++n)
+                if (!(d->inv_mass[n] > 0.f)) {
+                    const int64_t g = h->gidx(n);
+                    bits[g >> 5] |= 1u << (g & 31);
+                }
+        }
         CK(dalloc(&h->pinbits, words));
         CK(cudaMemcpyAsync(h->pinbits, bits.data(), words * 4, cudaMemcpyHostToDevice, h->st));
+        CK(cudaStreamSynchronize(h->st));  // `bits` goes out of scope
     }
     CK(dalloc(&h->inv_mass, P));  // storage layout (the respond pass reads it too)
     CK(cudaMemsetAsync(h->inv_mass, 0, P * 4, h->st));
-    if (int r = upload_planes<float>(h, d->inv_mass, h->inv_mass, 1)) return r;
+    if (gen) {
+        k_fill_inv_mass<<<nb(N), 256, 0, h->st>>>(h->rows, h->nx, h->pitch, gen->inv_mass, h->pinbits,
+                                                  h->inv_mass);
+        CK(cudaGetLastError());
+    } else if (int r = upload_planes<float>(h, d->inv_mass, h->inv_mass, 1)) {
+        return r;
+    }
     if (h->fp64) {
         CK(dalloc(&h->mass64, N));
         CK(dalloc(&h->pinned8, N));
@@ -779,7 +829,7 @@ static int build(cs_engine *h, const cs_desc *d) {
     // ---- triangles, incidence CSR, edges ----
     h->nc = d->num_tris;
     h->ne = d->num_edges;
-    {
+    if (!gen) {  // a generated grid needs no triangle table (no obstacle, stencil normals)
         const int64_t C = h->nc;
         std::vector<int32_t> tg(3 * C);
         for (int64_t i = 0; i < 3 * C; ++i) {
@@ -953,6 +1003,90 @@ extern "C" int cs_create(const cs_desc *d, cs_engine **out) {
         return r;
     }
     *out = h;
+    return 0;
+}
+
+// A grid engine straight from generate_cloth_grid's parameters (mesh.py:
+// 223-317), every per-node / per-spring quantity generated on the device.
+extern "C" int cs_create_grid(const cs_grid_desc *g, cs_engine **out) {
+    if (!g || !out) return fail(CS_E_INVALID, "null argument");
+    *out = nullptr;
+    if (g->abi_version != CS_ABI_VERSION) return fail(CS_E_INVALID, "ABI version mismatch");
+    if (g->nx < 2 || g->ny < 2) return fail(CS_E_INVALID, "grid needs at least 2 nodes per side");
+    if (!(g->width > 0.0) || !(g->height > 0.0)) return fail(CS_E_INVALID, "cloth dimensions must be positive");
+    if (!(g->total_mass > 0.0)) return fail(CS_E_INVALID, "total_mass must be positive");
+    const int row0 = g->row_lo, rows = g->row_hi - g->row_lo;
+    if (row0 < 0 || g->row_hi > g->ny || rows < 2) return fail(CS_E_INVALID, "local rows out of range");
+    if (g->flags & (CS_FLAG_FP64 | CS_FLAG_FORCE_CSR))
+        return fail(CS_E_INVALID, "generated grids run the float32 stencil (fast or fixed)");
+    if (g->num_pinned_rows > 0 && !g->pinned_rows) return fail(CS_E_INVALID, "pinned_rows missing");
+    if ((int64_t)g->nx * rows > ((int64_t)1 << 31) - 1) return fail(CS_E_CAPACITY, "more than 2^31-1 nodes");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(CS_E_NODEVICE, "no CUDA device is available");
+    }
+    GridGen gen;
+    gen.nx = g->nx;
+    gen.ny = g->ny;
+    gen.row0 = row0;
+    gen.width = g->width;
+    gen.height = g->height;
+    gen.orient = g->orientation;
+    const double m = g->total_mass / ((double)g->nx * g->ny);  // mesh.py:258
+    gen.inv_mass = (float)(1.0 / m);                           // engine.py:199-202
+    for (int k = 0; k < g->num_pinned_rows; ++k) {
+        if (g->pinned_rows[k] < 0 || g->pinned_rows[k] >= g->ny)
+            return fail(CS_E_INVALID, "pinned row index out of range");
+        gen.pinned_rows.push_back(g->pinned_rows[k]);
+    }
+    cs_desc d;
+    memset(&d, 0, sizeof d);
+    d.abi_version = CS_ABI_VERSION;
+    d.flags = g->flags;
+    d.nx = g->nx;
+    d.ny = rows;
+    bool uniform = true;
+    const cudaError_t e = grid_rest6(g->nx, g->ny, row0, rows, g->width, g->height, d.grid_rest,
+                                     &uniform, (cudaStream_t)g->stream);
+    if (e != cudaSuccess) return fail(CS_E_CUDA, std::string("grid rest lengths: ") + cudaGetErrorString(e));
+    if (!uniform)
+        return fail(CS_E_INVALID, "a spring family of this grid has more than one float32 rest "
+                                  "length; build the engine from the mesh instead");
+    d.num_nodes = (int64_t)g->nx * rows;
+    d.num_tris = 2 * (int64_t)(g->nx - 1) * (rows - 1);
+    d.dt = g->dt;
+    for (int q = 0; q < 3; ++q) {
+        d.gravity[q] = g->gravity[q];
+        d.stiffness[q] = g->stiffness[q];
+    }
+    d.damping = g->damping;
+    d.epsilon_mt = g->epsilon_mt;
+    d.response_margin = g->response_margin;
+    d.fixed_point_scale = g->fixed_point_scale;
+    d.substeps = g->substeps;
+    d.stream = g->stream;
+    cs_engine *h = new cs_engine();
+    int r = build(h, &d, &gen);
+    if (r) {
+        std::string keep = g_err;
+        cudaGetLastError();
+        cs_destroy(h);
+        g_err = keep;
+        return r;
+    }
+    *out = h;
+    return 0;
+}
+
+extern "C" int cs_grid_topology(int32_t nx, int32_t ny, int32_t row_lo, int32_t row_hi,
+                                double width, double height, int32_t *springs, int32_t *kinds,
+                                double *rest, int32_t *tris, double *positions, void *stream) {
+    if (nx < 2 || ny < 2 || row_lo < 0 || row_hi > ny || row_hi - row_lo < 2)
+        return fail(CS_E_INVALID, "bad grid / rows");
+    const cudaError_t e = grid_topology(nx, ny, row_lo, row_hi - row_lo, width, height, springs,
+                                        kinds, rest, tris, positions, (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(CS_E_CUDA, cudaGetErrorString(e));
     return 0;
 }
 

@@ -249,6 +249,58 @@ def pinned_empty(shape, dtype=np.float32) -> np.ndarray:
         return np.empty(shape, dtype=dtype)
 
 
+def _engine_flags(p, precision, graph, force_csr, kernel, normals, narrow, seam) -> int:
+    """cs_desc.flags of an Engine's keyword options."""
+    flags = 0
+    if p.explicit_euler:
+        flags |= N.FLAG_EXPLICIT_EULER
+    if p.average_response:
+        flags |= N.FLAG_AVERAGE_RESPONSE
+    if precision == "fixed":
+        flags |= N.FLAG_FIXED_POINT
+    if precision == "fp64":
+        flags |= N.FLAG_FP64
+    if not graph:
+        flags |= N.FLAG_NO_GRAPH
+    if force_csr:
+        flags |= N.FLAG_FORCE_CSR
+    if kernel not in ("strip", "pair", "tile"):
+        raise ValueError("kernel must be 'pair' (paired-column f32x2 warp strips, default), "
+                         "'strip' (scalar warp strips) or 'tile' (shared-memory tiles)")
+    if kernel == "tile":
+        flags |= N.FLAG_TILE_KERNEL
+    if normals not in ("auto", "fused", "split"):
+        raise ValueError("normals must be 'auto', 'fused' (inside the next frame's step "
+                         "kernel) or 'split' (stand-alone kernel after each step)")
+    flags |= {"auto": 0, "split": N.FLAG_SPLIT_NORMALS, "fused": N.FLAG_FUSE_NORMALS}[normals]
+    if narrow not in ("tri", "batch", "warp", "thread"):
+        raise ValueError("narrow must be 'tri' (one fused candidate enumeration per cloth "
+                         "triangle for both passes, default), 'batch' (batched queries per "
+                         "pass), 'warp' (warp per query) or 'thread' (thread per query)")
+    if narrow == "thread":
+        flags |= N.FLAG_THREAD_NARROW
+    elif narrow == "warp":
+        flags |= N.FLAG_WARP_NARROW
+    elif narrow == "batch":
+        flags |= N.FLAG_SPLIT_NARROW
+    if kernel == "pair":
+        flags |= N.FLAG_PAIRED
+    if seam not in ("kernel", "stream"):
+        raise ValueError("seam must be 'kernel' (row-band handshake inside the step kernel, "
+                         "graph-replayed frames) or 'stream' (stream waits on flag words)")
+    if seam == "stream":
+        flags |= N.FLAG_MEMOP_SEAM
+    return flags
+
+
+def _stream_handle(stream) -> int:
+    handle = int(getattr(stream, "cuda_stream", stream))
+    if handle == 0:
+        raise ValueError("pass a non-default CUDA stream (the legacy default stream "
+                         "handle 0 means 'let the engine create its own')")
+    return handle
+
+
 class Engine:
     """A built B200 pipeline bound to one cloth/obstacle/params configuration."""
 
@@ -313,15 +365,8 @@ class Engine:
                     rest32=np.ascontiguousarray(np.asarray(mesh.spring_rest_lengths).astype(_F32)))
         d = N.CsDesc()
         d.abi_version = N.ABI_VERSION
-        flags = 0
-        if p.explicit_euler:
-            flags |= N.FLAG_EXPLICIT_EULER
-        if p.average_response:
-            flags |= N.FLAG_AVERAGE_RESPONSE
-        if precision == "fixed":
-            flags |= N.FLAG_FIXED_POINT
+        flags = _engine_flags(p, precision, graph, force_csr, kernel, normals, narrow, seam)
         if precision == "fp64":
-            flags |= N.FLAG_FP64
             keep["pos64"] = np.ascontiguousarray(mesh.positions, dtype=np.float64)
             keep["mass64"] = np.ascontiguousarray(masses)
             keep["pin8"] = np.ascontiguousarray(pinned.astype(np.uint8))
@@ -330,36 +375,6 @@ class Engine:
             d.masses64 = _p(keep["mass64"])
             d.pinned = _p(keep["pin8"])
             d.spring_rest64 = _p(keep["rest64"])
-        if not graph:
-            flags |= N.FLAG_NO_GRAPH
-        if force_csr:
-            flags |= N.FLAG_FORCE_CSR
-        if kernel not in ("strip", "pair", "tile"):
-            raise ValueError("kernel must be 'pair' (paired-column f32x2 warp strips, default), "
-                             "'strip' (scalar warp strips) or 'tile' (shared-memory tiles)")
-        if kernel == "tile":
-            flags |= N.FLAG_TILE_KERNEL
-        if normals not in ("auto", "fused", "split"):
-            raise ValueError("normals must be 'auto', 'fused' (inside the next frame's step "
-                             "kernel) or 'split' (stand-alone kernel after each step)")
-        flags |= {"auto": 0, "split": N.FLAG_SPLIT_NORMALS, "fused": N.FLAG_FUSE_NORMALS}[normals]
-        if narrow not in ("tri", "batch", "warp", "thread"):
-            raise ValueError("narrow must be 'tri' (one fused candidate enumeration per cloth "
-                             "triangle for both passes, default), 'batch' (batched queries per "
-                             "pass), 'warp' (warp per query) or 'thread' (thread per query)")
-        if narrow == "thread":
-            flags |= N.FLAG_THREAD_NARROW
-        elif narrow == "warp":
-            flags |= N.FLAG_WARP_NARROW
-        elif narrow == "batch":
-            flags |= N.FLAG_SPLIT_NARROW
-        if kernel == "pair":
-            flags |= N.FLAG_PAIRED
-        if seam not in ("kernel", "stream"):
-            raise ValueError("seam must be 'kernel' (row-band handshake inside the step kernel, "
-                             "graph-replayed frames) or 'stream' (stream waits on flag words)")
-        if seam == "stream":
-            flags |= N.FLAG_MEMOP_SEAM
         d.flags = flags
         if stencil is not None:
             d.nx, d.ny = stencil[0], stencil[1]
@@ -401,11 +416,7 @@ class Engine:
         d.substeps = int(p.substeps)
         d.cell_size = float(cell_size) if cell_size else 0.0
         if stream is not None:
-            handle = int(getattr(stream, "cuda_stream", stream))
-            if handle == 0:
-                raise ValueError("pass a non-default CUDA stream (the legacy default stream "
-                                 "handle 0 means 'let the engine create its own')")
-            d.stream = handle
+            d.stream = _stream_handle(stream)
         h = ctypes.c_void_p()
         N.check(self._lib.cs_create(ctypes.byref(d), ctypes.byref(h)))
         self._handle = h
@@ -415,6 +426,77 @@ class Engine:
         self.frame_count = 0
         self.buffers = PipelineBuffers(self)
         self._has_obstacle = has_obs
+
+    @classmethod
+    def from_grid(cls, nx: int, ny: int, params=None, *, width: float = 1.0,
+                  height: float = 1.0, total_mass: float | None = None, pinned_rows="first",
+                  orientation: str = "hanging", row_lo: int = 0, row_hi: int | None = None,
+                  device=None, precision: str = "fast", graph: bool = True, stream=None,
+                  kernel: str = "pair", normals: str = "auto", seam: str = "kernel"):
+        """An engine for generate_cloth_grid(nx, ny, width, height, total_mass,
+        pinned_rows) (mesh.py:223-317) -- rows [row_lo, row_hi) of it for a
+        row band -- generated on the device (cs_create_grid): no per-node or
+        per-spring array is built on the host.  orientation "hanging" applies
+        the hanging scene's rotation (scenes.py _rotate_xz_to_xy), "xz" keeps
+        the generation plane.  Fast or fixed arithmetic (the float64 mode
+        needs the mesh's arrays: Engine(mesh, ...))."""
+        if precision not in ("fast", "fixed"):
+            raise ValueError("Engine.from_grid builds fast or fixed engines")
+        if orientation not in ("hanging", "xz"):
+            raise ValueError("orientation must be 'hanging' or 'xz'")
+        from .mesh import GridCloth
+
+        row_hi = ny if row_hi is None else row_hi
+        cloth = GridCloth(nx, ny, width, height, total_mass, pinned_rows, row_lo, row_hi,
+                          orientation)
+        self = cls.__new__(cls)
+        self.mesh, self.obstacle = cloth, None
+        self.params = params if params is not None else SimParams()
+        self.device = device if device is not None else get_adapter()
+        self.pair_budget = DEFAULT_PAIR_BUDGET
+        self.precision = precision
+        self._lib = N.load()
+        self._handle = None
+        p = self.params
+        n = cloth.num_nodes
+        pitch_nodes = ((nx + 31) // 32 * 32) * (row_hi - row_lo)
+        state_bytes = 2 * 6 * pitch_nodes * 4
+        self.layout = Layout(n, cloth.num_springs, cloth.num_triangles,
+                             cloth.num_unique_edges, 0, state_bytes,
+                             state_bytes + 3 * pitch_nodes * 4 + 24 * pitch_nodes)
+        free, _ = self.device.mem_info()
+        self.layout.validate(free)
+        self.pairs_per_frame = 0
+        g = N.CsGridDesc()
+        g.abi_version = N.ABI_VERSION
+        g.flags = _engine_flags(p, precision, graph, False, kernel, normals, "tri", seam)
+        g.nx, g.ny, g.row_lo, g.row_hi = nx, ny, row_lo, row_hi
+        g.width, g.height, g.total_mass = width, height, cloth.total_mass
+        g.orientation = 1 if orientation == "hanging" else 0
+        rows = np.ascontiguousarray(cloth.pinned_row_list, dtype=np.int32)
+        g.num_pinned_rows = len(rows)
+        g.pinned_rows = rows.ctypes.data if len(rows) else None
+        g.dt = p.dt / p.substeps
+        for q in range(3):
+            g.gravity[q] = float(p.gravity[q])
+            g.stiffness[q] = float(p.stiffness[q])
+        g.damping = float(p.damping)
+        g.epsilon_mt = float(p.epsilon_mt)
+        g.response_margin = float(p.response_margin)
+        g.fixed_point_scale = int(p.fixed_point_scale)
+        g.substeps = int(p.substeps)
+        if stream is not None:
+            g.stream = _stream_handle(stream)
+        h = ctypes.c_void_p()
+        N.check(self._lib.cs_create_grid(ctypes.byref(g), ctypes.byref(h)))
+        self._handle = h
+        self.kparams = g
+        self.stencil = True
+        self._fused_normals = kernel != "tile" and normals != "split" and precision == "fast"
+        self.frame_count = 0
+        self.buffers = PipelineBuffers(self)
+        self._has_obstacle = False
+        return self
 
     # -- lifetime -----------------------------------------------------------------
     def close(self):

@@ -383,6 +383,66 @@ def grid_band(nx: int, ny: int, j0: int, j1: int, width: float = 1.0, height: fl
                      triangles=grid_triangles(nx, lny))
 
 
+class GridCloth:
+    """generate_cloth_grid's parameters without its arrays: what
+    Engine.from_grid builds on the device (cs_create_grid).  Rows
+    [row_lo, row_hi) of the nx x ny grid form the local sheet; the
+    ClothMesh arrays (positions in the chosen orientation, masses, pins,
+    springs, rest lengths, triangles) are built on the host only if
+    something asks for them."""
+
+    def __init__(self, nx, ny, width=1.0, height=1.0, total_mass=None, pinned_rows="first",
+                 row_lo=0, row_hi=None, orientation="hanging"):
+        if nx < 2 or ny < 2:
+            raise ValueError("grid needs at least 2 nodes per side")
+        self.full_nx, self.full_ny = nx, ny
+        self.row_lo, self.row_hi = row_lo, (ny if row_hi is None else row_hi)
+        if not (0 <= self.row_lo < self.row_hi <= ny) or self.row_hi - self.row_lo < 2:
+            raise ValueError(f"local rows [{row_lo}, {row_hi}) outside a grid of {ny} rows")
+        self.width, self.height = float(width), float(height)
+        self.total_mass = float(total_mass) if total_mass is not None else 0.05 * nx * ny
+        self.pinned_rows = pinned_rows
+        self.pinned_row_list = _resolve_pinned_rows(pinned_rows, ny)
+        self.orientation = orientation
+        self.nx, self.ny = nx, self.row_hi - self.row_lo
+        self._mesh = None
+
+    @property
+    def num_nodes(self) -> int:
+        return self.nx * self.ny
+
+    @property
+    def num_springs(self) -> int:
+        return sum(spring_count_formula(self.nx, self.ny))
+
+    @property
+    def num_triangles(self) -> int:
+        return 2 * (self.nx - 1) * (self.ny - 1)
+
+    @property
+    def num_unique_edges(self) -> int:
+        return (self.nx - 1) * self.ny + self.nx * (self.ny - 1) + (self.nx - 1) * (self.ny - 1)
+
+    def materialize(self) -> ClothMesh:
+        """The local sheet as a ClothMesh (host arrays, vectorised builders)."""
+        if self._mesh is None:
+            m = grid_band(self.full_nx, self.full_ny, self.row_lo, self.row_hi, self.width,
+                          self.height, total_mass=self.total_mass, pinned_rows=self.pinned_rows)
+            if self.orientation == "hanging":  # scenes._rotate_xz_to_xy
+                rot = np.zeros_like(m.positions)
+                rot[:, 0] = m.positions[:, 0]
+                rot[:, 1] = -m.positions[:, 2]
+                m.positions = rot
+            self._mesh = m
+        return self._mesh
+
+    def __getattr__(self, name):
+        if name in ("positions", "masses", "pinned", "spring_indices", "spring_rest_lengths",
+                    "spring_kinds", "triangles"):
+            return getattr(self.materialize(), name)
+        raise AttributeError(name)
+
+
 def band_of_mesh(mesh, nx: int, ny: int, rest6, j0: int, j1: int) -> ClothMesh:
     """Rows [j0, j1) of an nx x ny grid ClothMesh as a stand-alone sheet for
     a row band: the global node data of those rows, the grid topology of an

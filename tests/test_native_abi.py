@@ -58,6 +58,23 @@ def test_descriptor_layout_matches_c(tmp_path):
     assert int(out["peer_flag"]) == N.CsHaloPeer.remote_flag.offset
 
 
+def test_grid_descriptor_layout_matches_c(tmp_path):
+    src = tmp_path / "glayout.c"
+    fields = [f for f, _ in N.CsGridDesc._fields_]
+    body = "\n".join(f'printf("{f} %zu\\n", offsetof(cs_grid_desc, {f}));' for f in fields)
+    src.write_text(
+        "#include <stdio.h>\n#include <stddef.h>\n#include \"clothsim_b200.h\"\n"
+        "int main(void){\n" + body + '\nprintf("sizeof %zu\\n", sizeof(cs_grid_desc));\nreturn 0;}\n')
+    exe = tmp_path / "glayout"
+    cc = "/usr/bin/gcc" if os.path.exists("/usr/bin/gcc") else "gcc"
+    subprocess.run([cc, "-I", os.path.dirname(HEADER), str(src), "-o", str(exe)], check=True)
+    out = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True,
+                                                        text=True).stdout.splitlines())
+    for f in fields:
+        assert int(out[f]) == getattr(N.CsGridDesc, f).offset, f
+    assert int(out["sizeof"]) == ctypes.sizeof(N.CsGridDesc)
+
+
 def test_adapter_none_is_refused(monkeypatch):
     from paper_2507_11794_b200 import AdapterUnavailable, get_adapter
 
