@@ -11,6 +11,7 @@
 #include <climits>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -121,6 +122,21 @@ struct cs_engine {
         if (fixed && (flags & CS_FLAG_PAIRED)) return false;
         return true;
     }
+    // The exact paired frame's normals kernel (split, see above) computes the
+    // normals of the frame's starting state on a forked stream, concurrently
+    // with the force pass that reads the same state: both kernels are
+    // latency-bound with issue slots to spare.  The buffer then trails by one
+    // frame like the fused one (refreshed when read).  CS_NRM_OVERLAP=0
+    // restores the serial order.
+    bool lag_normals() const {
+        if (fuse_normals() || banded || !(grid && strip && fixed && (flags & CS_FLAG_PAIRED)))
+            return false;
+        const char *e = getenv("CS_NRM_OVERLAP");
+        return !(e && e[0] == '0');
+    }
+    bool normals_lagged() const { return fuse_normals() || lag_normals(); }
+    cudaStream_t nrm_st = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_nrm = nullptr;
     bool normals_stale = false; // normals buffer holds the previous frame's (fused)
     float *corners = nullptr, *onormals = nullptr;
     BroadPhase bp;
@@ -409,7 +425,11 @@ static void pass_respond(cs_engine *h) {
                    /*end_of_frame=*/true, h->st);
 }
 
-static void pass_normals(cs_engine *h) {
+static void pass_normals(cs_engine *h, cudaStream_t st = nullptr) {
+    if (st) {  // the exact paired kernel on a forked stream (cs_engine::lag_normals)
+        launch_pair_normals_exact(h->sp, (const float *)h->state[h->cur], (float *)h->normals, st);
+        return;
+    }
     if (h->fp64) {
         launch_csr_normals_f64(h->N, h->plane, h->nc, (const double *)h->state[h->cur], h->tris_g,
                                (double *)h->face, h->inc_off, h->inc_tri, (double *)h->normals, h->st);
@@ -435,14 +455,23 @@ static void launch_frame(cs_engine *h) {
     // concurrently with this frame's step measured 319.6 vs 321.6 us at
     // 4096^2 -- both kernels fill the SMs -- and was dropped; retried with
     // the TMA kernel at C2, where the SMs are not full: 22.6 vs 20.5 us.)
-    const bool fuse = h->fuse_normals();
+    const bool fuse = h->fuse_normals(), lag = h->lag_normals();
+    if (lag) {  // the starting state's normals, beside the force pass
+        cudaEventRecord(h->ev_fork, h->st);
+        cudaStreamWaitEvent(h->nrm_st, h->ev_fork, 0);
+        pass_normals(h, h->nrm_st);
+        cudaEventRecord(h->ev_nrm, h->nrm_st);
+    }
     pass_force_integrate(h, fuse);
     if (h->has_obstacle) {
         pass_detect(h);
         pass_respond(h);
     }
-    if (!fuse) pass_normals(h);
-    h->normals_stale = fuse;
+    if (lag)
+        cudaStreamWaitEvent(h->st, h->ev_nrm, 0);
+    else if (!fuse)
+        pass_normals(h);
+    h->normals_stale = fuse || lag;
 }
 
 // ---------------------------------------------------------------------------
@@ -967,6 +996,12 @@ extern "C" int cs_destroy(cs_engine *h) {
         cudaStreamSynchronize(h->copy_st);
         cudaStreamDestroy(h->copy_st);
     }
+    if (h->nrm_st) {
+        cudaStreamSynchronize(h->nrm_st);
+        cudaStreamDestroy(h->nrm_st);
+    }
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    if (h->ev_nrm) cudaEventDestroy(h->ev_nrm);
     if (h->clog) cudaFree(h->clog);
     if (h->clog_n) cudaFree(h->clog_n);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
@@ -1102,6 +1137,11 @@ extern "C" int cs_step(cs_engine *h, int32_t frames) {
         }
         return 0;
     }
+    if (h->lag_normals() && !h->nrm_st) {
+        CK(cudaStreamCreateWithFlags(&h->nrm_st, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h->ev_nrm, cudaEventDisableTiming));
+    }
     for (int32_t f = 0; f < frames; ++f) {
         if (h->use_graph) {
             const int start = h->cur;
@@ -1118,7 +1158,7 @@ extern "C" int cs_step(cs_engine *h, int32_t frames) {
             // replay the parity bookkeeping of one frame
             if (h->substeps & 1) h->cur = 1 - start;
             h->forces_valid = true;
-            h->normals_stale = h->fuse_normals();
+            h->normals_stale = h->normals_lagged();
         } else {
             launch_frame(h);
             CK(cudaGetLastError());

@@ -326,3 +326,38 @@ def test_strided_batches_of_every_size_equal_warp_per_query(n):
         assert a.stats()["hit_counter"] == b.stats()["hit_counter"] > 0
         np.testing.assert_array_equal(a.read_positions(), b.read_positions())
         np.testing.assert_array_equal(key(ca), key(b.read_contacts()))
+
+
+@pytest.mark.parametrize("stiffness", [None, 1e9])
+def test_fixed_mode_spring_guard_edges(stiffness):
+    """The exact step kernel takes its inline fast path (inline sqrt, shared
+    reciprocal, magic-number rint) only inside a per-spring guard; every
+    edge of that guard against the reference engine, bit for bit: coincident
+    nodes (|d| = 0), |d| < 1e-12, a component below 2^-60 beside a normal
+    length, forces above 2^22 / scale (64 N) and -- at k = 1e9 -- beyond the
+    i32 saturation, and a NaN velocity (encoded to 0)."""
+    sc = P.build_scene(P.ScenarioConfig("hanging", (70, 33), dt=0.004))
+    params = sc.params if stiffness is None else P.SimParams(
+        dt=sc.params.dt, stiffness=stiffness, damping=sc.params.damping)
+    rng = np.random.default_rng(11)
+    n, nx = sc.mesh.num_nodes, 70
+    pos = (sc.mesh.positions + rng.normal(scale=2e-3, size=(n, 3))).astype(np.float32)
+    vel = rng.normal(scale=0.05, size=(n, 3)).astype(np.float32)
+    pos[5 * nx + 5] = pos[5 * nx + 6]                                   # coincident
+    pos[7 * nx + 9] = pos[7 * nx + 10] + np.float32(1e-13)              # |d| < 1e-12
+    pos[9 * nx + 20] = pos[9 * nx + 21] + np.array([1e-20, 0.01, 0.0], np.float32)
+    pos[20 * nx + 30: 20 * nx + 34] += np.float32(2.0)                  # |F| >> 64 N
+    vel[25 * nx + 40] = np.nan
+    eng = P.Engine(sc.mesh, params=params, precision="fixed")
+    eng.write_positions(pos)
+    eng.write_velocities(vel)
+    eo = O.EngineOracle(sc.mesh, params)
+    eo.pos[...] = pos
+    eo.vel[...] = vel
+    for _ in range(3):
+        eng.step()
+        eo.step()
+        np.testing.assert_array_equal(eng.read_forces_raw(), eo.forces)
+        np.testing.assert_array_equal(eng.read_positions(), eo.pos)
+        np.testing.assert_array_equal(eng.read_velocities(), eo.vel)
+    np.testing.assert_array_equal(eng.read_normals(), eo.normals)
