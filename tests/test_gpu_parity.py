@@ -361,3 +361,31 @@ def test_fixed_mode_spring_guard_edges(stiffness):
         np.testing.assert_array_equal(eng.read_positions(), eo.pos)
         np.testing.assert_array_equal(eng.read_velocities(), eo.vel)
     np.testing.assert_array_equal(eng.read_normals(), eo.normals)
+
+
+def test_fixed_mode_normals_guard_edges():
+    """The exact normals kernel's guarded fast path against the reference
+    engine's normal_update, bit for bit: a crumpled sheet with collapsed
+    triangles (zero cross products), tiny ones (|f|^2 below 2^-101),
+    collinear nodes, huge coordinates (|f|^2 overflows) and a NaN node."""
+    sc = P.build_scene(P.ScenarioConfig("hanging", (70, 33), dt=0.004))
+    rng = np.random.default_rng(5)
+    n, nx = sc.mesh.num_nodes, 70
+    pos = (sc.mesh.positions + rng.normal(scale=3e-3, size=(n, 3))).astype(np.float32)
+    pos[3 * nx + 3] = pos[3 * nx + 4]                                   # collapsed
+    pos[4 * nx + 10: 4 * nx + 14] = pos[4 * nx + 10]                    # a collapsed run
+    base = pos[10 * nx + 20].copy()
+    pos[10 * nx + 20: 10 * nx + 23] = base + (rng.normal(size=(3, 3)) * 1e-17).astype(np.float32)
+    pos[11 * nx + 20: 11 * nx + 23] = base + (rng.normal(size=(3, 3)) * 1e-17).astype(np.float32)
+    pos[15 * nx + 5: 15 * nx + 9, 1] = pos[15 * nx + 5, 1]              # collinear row piece
+    pos[15 * nx + 5: 15 * nx + 9, 2] = pos[15 * nx + 5, 2]
+    pos[20 * nx + 50] = np.float32(3e19)                                # |f|^2 overflows
+    pos[25 * nx + 60] = np.nan
+    eng = P.Engine(sc.mesh, params=sc.params, precision="fixed")
+    eng.write_positions(pos)
+    eo = O.EngineOracle(sc.mesh, sc.params)
+    eo.pos[...] = pos
+    eo.update_normals()
+    from paper_2507_11794_b200 import _native as N
+    N.check(eng._lib.cs_run_pass(eng._handle, N.PASS_NORMALS))  # the normals of the written state
+    np.testing.assert_array_equal(eng.read_normals(), eo.normals)
