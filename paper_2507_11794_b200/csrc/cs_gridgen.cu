@@ -38,11 +38,18 @@ __device__ __forceinline__ double rest_len(double xa, double za, double xb, doub
     return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
 }
 
-// ordered-int keys of non-negative floats (rest lengths are >= 0)
-__device__ __forceinline__ void minmax(unsigned *mm, int fam, float v) {
+// ordered-int keys of non-negative floats (rest lengths are >= 0); reduced
+// across the warp first (one atomic pair per warp and family: per-thread
+// atomics on the 12 words took 0.5 ms at 4096^2); `has` = this lane has a
+// spring of the family (the call is warp-uniform)
+__device__ __forceinline__ void minmax(unsigned *mm, int fam, float v, bool has) {
     const unsigned k = __float_as_uint(v);
-    atomicMin(mm + 2 * fam, k);
-    atomicMax(mm + 2 * fam + 1, k);
+    const unsigned lo = __reduce_min_sync(0xffffffffu, has ? k : 0xffffffffu);
+    const unsigned hi = __reduce_max_sync(0xffffffffu, has ? k : 0u);
+    if ((threadIdx.x & 31) == 0 && lo != 0xffffffffu) {
+        atomicMin(mm + 2 * fam, lo);
+        atomicMax(mm + 2 * fam + 1, hi);
+    }
 }
 
 // Positions (f32 planes x y z at pitch layout) of local rows [0, rows) =
@@ -79,19 +86,18 @@ __global__ void k_grid_positions(int nx, int ny, int row0, int rows, double widt
 __global__ void k_grid_rest_minmax(int nx, int ny, int row0, int rows, double width,
                                    double height, unsigned *__restrict__ mm) {
     const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (n >= (int64_t)nx * rows) return;
-    const int i = (int)(n % nx), lj = (int)(n / nx), j = row0 + lj;
+    const bool v = n < (int64_t)nx * rows;  // every lane stays for the warp reductions
+    const int i = v ? (int)(n % nx) : 0, lj = v ? (int)(n / nx) : 0, j = row0 + lj;
     const double x0 = lin(i, nx, width), z0 = lin(j, ny, height);
-    const bool i1 = i + 1 < nx, j1 = lj + 1 < rows, i2 = i + 2 < nx, j2 = lj + 2 < rows;
+    const bool i1 = v && i + 1 < nx, j1 = v && lj + 1 < rows, i2 = v && i + 2 < nx,
+               j2 = v && lj + 2 < rows;
     const double x1 = i1 ? lin(i + 1, nx, width) : 0.0, z1 = j1 ? lin(j + 1, ny, height) : 0.0;
-    if (i1) minmax(mm, 0, (float)rest_len(x0, z0, x1, z0));
-    if (j1) minmax(mm, 1, (float)rest_len(x0, z0, x0, z1));
-    if (i1 && j1) {
-        minmax(mm, 2, (float)rest_len(x0, z0, x1, z1));   // (i, j) -> (i+1, j+1)
-        minmax(mm, 3, (float)rest_len(x1, z0, x0, z1));   // (i+1, j) -> (i, j+1)
-    }
-    if (i2) minmax(mm, 4, (float)rest_len(x0, z0, lin(i + 2, nx, width), z0));
-    if (j2) minmax(mm, 5, (float)rest_len(x0, z0, x0, lin(j + 2, ny, height)));
+    minmax(mm, 0, i1 ? (float)rest_len(x0, z0, x1, z0) : 0.f, i1);
+    minmax(mm, 1, j1 ? (float)rest_len(x0, z0, x0, z1) : 0.f, j1);
+    minmax(mm, 2, (i1 && j1) ? (float)rest_len(x0, z0, x1, z1) : 0.f, i1 && j1);  // (i,j)->(i+1,j+1)
+    minmax(mm, 3, (i1 && j1) ? (float)rest_len(x1, z0, x0, z1) : 0.f, i1 && j1);  // (i+1,j)->(i,j+1)
+    minmax(mm, 4, i2 ? (float)rest_len(x0, z0, lin(i + 2, nx, width), z0) : 0.f, i2);
+    minmax(mm, 5, j2 ? (float)rest_len(x0, z0, x0, lin(j + 2, ny, height)) : 0.f, j2);
 }
 
 // generate_cloth_grid's spring / triangle arrays of the local sheet (nx x
