@@ -1480,6 +1480,13 @@ static int join(cs_engine *h, cudaStream_t from, cudaStream_t to) {
     return 0;
 }
 
+#ifdef CS_PAIR3_TRACE
+namespace cs { int pair3_trace_read(unsigned long long *out, int n); }
+// diagnostic builds only: per-warp {start, end, smid} of the last k_pair3 launch
+extern "C" int cs_debug_pair3_trace(unsigned long long *out, int32_t n) {
+    return cs::pair3_trace_read(out, n);
+}
+#endif
 extern "C" int cs_device(cs_engine *h, int32_t *device) {
     if (!h || !device) return fail(CS_E_INVALID, "null argument");
     *device = h->device;

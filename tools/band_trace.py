@@ -1,0 +1,61 @@
+"""Per-warp timeline of one k_pair3 launch (diagnostic build with
+-DCS_PAIR3_TRACE: tools/ab_build.py trace -DCS_PAIR3_TRACE, then
+CLOTHSIM_LIB=.../var_trace.so): start / end spread, per-SM load and the
+share of the launch that is ramp-up and tail.
+
+    python tools/band_trace.py [world, default 8]  (a plain middle band of C5)
+    python tools/band_trace.py 1                   (the whole sheet)
+"""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+
+import paper_2507_11794_b200 as P
+from paper_2507_11794_b200 import _native as N
+from paper_2507_11794_b200.bands import BandedEngine
+from paper_2507_11794_b200.scenes import CONTACT_DT, NODE_MASS, stable_coefficients
+
+world = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+kk, cc = stable_coefficients(NODE_MASS, CONTACT_DT)
+params = P.SimParams(dt=CONTACT_DT, stiffness=kk, damping=cc)
+if world > 1:
+    eng = BandedEngine(4096, 4096, params, 1, world, exchange="p2p").engine
+else:
+    eng = P.Engine.from_grid(4096, 4096, params)
+eng.step_frames(20)
+eng.synchronize()
+lib = N.load()
+buf = np.zeros((1 << 16, 3), dtype=np.uint64)
+lib.cs_debug_pair3_trace.argtypes = [ctypes.c_void_p, ctypes.c_int32]
+assert lib.cs_debug_pair3_trace(buf.ctypes.data, 1 << 16) == 0
+t = buf[buf[:, 1] > 0]
+t0 = t[:, 0].min()
+start, end = (t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3
+sm, slot = t[:, 2] // 256, t[:, 2] % 256
+dur = end - start
+print(f"world {world}: {len(t)} warps, launch span {end.max():.2f} us")
+print(f"  start: median {np.median(start):.2f}  p99 {np.percentile(start, 99):.2f}  max {start.max():.2f} us")
+print(f"  end:   min {end.min():.2f}  median {np.median(end):.2f}  p99 {np.percentile(end, 99):.2f}  max {end.max():.2f} us")
+print(f"  warp duration: min {dur.min():.2f}  median {np.median(dur):.2f}  max {dur.max():.2f} us")
+per_sm = np.bincount(sm.astype(int))
+print(f"  warps per SM: min {per_sm[per_sm > 0].min()}  max {per_sm.max()}  SMs used {np.count_nonzero(per_sm)}")
+# per sub-partition (SMSP = warp slot % 4): warps sharing it and their end times
+part = sm.astype(int) * 4 + (slot.astype(int) % 4)
+load = np.bincount(part, minlength=int(part.max()) + 1)
+print("  warps per SMSP:", dict(zip(*np.unique(load[load > 0], return_counts=True))))
+for k in sorted(set(load[part])):
+    sel = load[part] == k
+    print(f"    SMSP with {k} warps: {sel.sum()} warps, end median {np.median(end[sel]):.2f} max {end[sel].max():.2f} us,"
+          f" duration median {np.median(dur[sel]):.2f}")
+rows = eng_rows = None
+busy = np.zeros(int(end.max() * 10) + 2)
+for s_, e_ in zip(start, end):
+    busy[int(s_ * 10):int(e_ * 10)] += 1
+cap = busy.max()
+print(f"  resident warps over time (0.1 us bins): peak {cap:.0f}; mean/peak {busy.mean() / cap:.3f}")
+for q in (0.1, 0.25, 0.5, 0.75, 0.9, 1.0):
+    i = int(q * (len(busy) - 1))
+    print(f"    t={i / 10:6.2f} us  resident {busy[i]:.0f}")
