@@ -50,7 +50,14 @@ for k in sorted(set(load[part])):
     sel = load[part] == k
     print(f"    SMSP with {k} warps: {sel.sum()} warps, end median {np.median(end[sel]):.2f} max {end[sel].max():.2f} us,"
           f" duration median {np.median(dur[sel]):.2f}")
-rows = eng_rows = None
+ends = {}
+for pi, e in zip(part, end):
+    ends.setdefault(int(pi), []).append(float(e))
+for k in (2, 3, 4, 5, 6):
+    grp = [sorted(v) for v in ends.values() if len(v) == k]
+    if grp:
+        m = np.mean(np.array(grp), axis=0)
+        print(f"    SMSPs with {k} warps ({len(grp)}): mean k-th end times " + ", ".join(f"{x:.2f}" for x in m))
 busy = np.zeros(int(end.max() * 10) + 2)
 for s_, e_ in zip(start, end):
     busy[int(s_ * 10):int(e_ * 10)] += 1
