@@ -5,6 +5,7 @@ share of the launch that is ramp-up and tail.
 
     python tools/band_trace.py [world, default 8]  (a plain middle band of C5)
     python tools/band_trace.py 1                   (the whole sheet)
+    python tools/band_trace.py 8 linked            (self-linked, in-kernel seam)
 """
 import ctypes
 import os
@@ -19,18 +20,33 @@ from paper_2507_11794_b200.bands import BandedEngine
 from paper_2507_11794_b200.scenes import CONTACT_DT, NODE_MASS, stable_coefficients
 
 world = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+linked = len(sys.argv) > 2 and sys.argv[2] == "linked"
 kk, cc = stable_coefficients(NODE_MASS, CONTACT_DT)
 params = P.SimParams(dt=CONTACT_DT, stiffness=kk, damping=cc)
-if world > 1:
+if world > 1 and linked:
+    # the self-linked middle band of tools/band_overhead.py (in-kernel seam)
+    from paper_2507_11794_b200.bands import HaloPlan
+    me = BandedEngine(4096, 4096, params, 1, world, exchange="p2p", seam="kernel")
+    dummy = BandedEngine(4096, 4096, params, 1, world, exchange="p2p", seam="kernel")
+    mine, info = me.buffers(), dummy.buffers()
+    up = (dict(info, flags=mine["flags"] - 4), HaloPlan(4096, world, 0))
+    down = (dict(info, flags=mine["flags"] + 4), HaloPlan(4096, world, 2)) if world > 2 else None
+    me.link(up, down)
+    eng = me.engine
+    me.step(20)
+elif world > 1:
     eng = BandedEngine(4096, 4096, params, 1, world, exchange="p2p").engine
+    eng.step_frames(20)
 else:
     eng = P.Engine.from_grid(4096, 4096, params)
-eng.step_frames(20)
+    eng.step_frames(20)
 eng.synchronize()
 lib = N.load()
-buf = np.zeros((1 << 16, 3), dtype=np.uint64)
+raw = np.zeros((1 << 16) * 7, dtype=np.uint64)
 lib.cs_debug_pair3_trace.argtypes = [ctypes.c_void_p, ctypes.c_int32]
-assert lib.cs_debug_pair3_trace(buf.ctypes.data, 1 << 16) == 0
+assert lib.cs_debug_pair3_trace(raw.ctypes.data, 1 << 16) == 0
+buf = raw[: 3 << 16].reshape(-1, 3)
+stamps = raw[3 << 16:].reshape(-1, 4)
 t = buf[buf[:, 1] > 0]
 t0 = t[:, 0].min()
 start, end = (t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3
@@ -50,6 +66,21 @@ for k in sorted(set(load[part])):
     sel = load[part] == k
     print(f"    SMSP with {k} warps: {sel.sum()} warps, end median {np.median(end[sel]):.2f} max {end[sel].max():.2f} us,"
           f" duration median {np.median(dur[sel]):.2f}")
+strips = (4096 + 59) // 60
+sy = np.nonzero(buf[:, 1] > 0)[0] // strips
+for name, sel in (("seam chunk rows (sy 0, 1)", sy <= 1), ("interior", sy > 1)):
+    if sel.any():
+        print(f"  {name}: {sel.sum()} warps, duration median {np.median(dur[sel]):.2f} max {dur[sel].max():.2f},"
+              f" end median {np.median(end[sel]):.2f} max {end[sel].max():.2f} us")
+if linked:
+    st = stamps[np.nonzero(buf[:, 1] > 0)[0]].astype(np.int64)
+    rel = lambda a: (a - t[:, 0].astype(np.int64)) / 1e3
+    w0, lp, ep, sg = rel(st[:, 0]), rel(st[:, 1]), rel(st[:, 2]), rel(st[:, 3])
+    for name, sel in (("seam warps", sy <= 1), ("interior warps", sy > 1)):
+        print(f"  {name} ({sel.sum()}), medians after their start: wait done {np.median(w0[sel]):.2f},"
+              f" row loop done {np.median(lp[sel]):.2f}"
+              + (f", epilogue done {np.median(ep[sel]):.2f}" if (st[sel, 2] > 0).all() else "")
+              + f", signal done {np.median(sg[sel]):.2f} us")
 ends = {}
 for pi, e in zip(part, end):
     ends.setdefault(int(pi), []).append(float(e))
