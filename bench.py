@@ -122,6 +122,20 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def host_cpu():
+    """The host CPU model and logical core count (state them)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "host_logical_cpus": os.cpu_count()}
+
+
 def cpu_baseline(scene, seconds=15.0, max_steps=200):
     """Time the oracle's float64 solver step (restatement of solver.step) on
     this host's cores on the same workload."""
@@ -137,7 +151,7 @@ def cpu_baseline(scene, seconds=15.0, max_steps=200):
         so.step()
         k += 1
     dt = time.perf_counter() - t0
-    return {"value": k / dt, "unit": "steps/s", "cores": threads, "kind": "port",
+    return {"value": k / dt, "unit": "steps/s", "cores": threads, "kind": "port", **host_cpu(),
             "sample": f"{k} consecutive solver steps of the same workload ({dt:.1f} s, "
                       f"oracle/clothsim_oracle.c f64, {threads} threads)",
             "node_updates_per_s": k * scene.mesh.num_nodes / dt}
@@ -184,6 +198,7 @@ def run_reference(args, scene, config_name):
         "config": {"workload": f"{config_name}: {BASELINE_CONFIGS[config_name]}", "nodes": n_full},
         "node_updates_per_s": v * n_full,
         "cpu_baseline": {"value": v, "unit": "steps/s", "cores": threads, "kind": "port",
+                         **host_cpu(),
                          "sample": f"{done} steps of oracle/ (restated float64 solver.step), "
                                    f"{note}, after {args.warmup} warm-up"},
         "e2e": {"value": v, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -576,7 +591,7 @@ def collision_cpu_baseline(scene, positions, seconds=20.0):
     t_b = 3 * T * C / rates["pass_b"]["pairs_per_s"]
     frame = t_step + t_a + t_b
     return {"value": 1.0 / frame, "unit": "steps/s", "cores": threads, "kind": "port",
-            "extrapolated": True,
+            "extrapolated": True, **host_cpu(),
             "sample": (f"oracle/ float64 solver.step restatement, {threads} threads: pass A "
                        f"{rates['pass_a']['slice']}, pass B {rates['pass_b']['slice']} (measured "
                        f"pairs/s at the draped GPU state), {k} spring+integrate steps; frame = "
