@@ -6,6 +6,8 @@
 #     c5_frame   C5 fused frame (k_pair3<NORMALS=1>)
 #     c5_split   C5 stand-alone normals + force pass (k_pair_normals, k_pair3<0>)
 #     c3_draped  C3 narrow phase + respond of a draped frame (after 200 frames)
+#     c2_fixed   C2 exact pair: k_pair_normals_x + guarded exact k_pair3<0,0,0,1>
+#     band8      8-way band of C5, self-linked: BAND k_pair3 with the in-kernel seam
 #   Everything lands in gpurun_out/; tools/update_profiles.py copies it.
 set -u
 O=gpurun_out
@@ -20,4 +22,8 @@ $NCU -k regex:k_pair3 -c 1 -o $O/c5_frame python tools/prof_kernels.py C5 1 > $O
 # (k_pair_normals) and then runs k_pair3<0>
 $NCU -k regex:k_pair -s 5 -c 2 -o $O/c5_split python tools/prof_kernels.py C5 1 > $O/ncu_c5s.log 2>&1
 $NCU -k regex:"k_detect|k_respond" -s 400 -c 2 -o $O/c3_draped python tools/prof_c3.py C3 1 > $O/ncu_c3.log 2>&1
+# prof_fixed: 3 graph frames (force + forked normals), then the force pass
+# (which first refreshes the lagged normals) -- skip 6, capture normals + force
+$NCU -k regex:k_pair -s 6 -c 2 -o $O/c2_fixed python tools/prof_fixed.py C2 2 > $O/ncu_fixed.log 2>&1
+$NCU -k regex:k_pair3 -s 2 -c 1 -o $O/band8 python tools/prof_band.py 8 4 > $O/ncu_band.log 2>&1
 ls -la $O

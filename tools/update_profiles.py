@@ -48,6 +48,10 @@ with open(os.path.join(P, f"{R}_ncu_summary.txt"), "w") as fh:
     fh.write("# C5 fused frame kernel (k_pair3<1,0>, 16.8M nodes)\n" + summary(os.path.join(G, "c5_frame.ncu-rep"), 1))
     fh.write("# C5 split passes: stand-alone k_pair_normals, then force+integrate k_pair3<0,0>\n" + summary(os.path.join(G, "c5_split.ncu-rep"), 2))
     fh.write("# C3 collision (draped: after 200 frames): fused narrow phase + respond\n" + summary(os.path.join(G, "c3_draped.ncu-rep")))
+    if os.path.exists(os.path.join(G, "c2_fixed.ncu-rep")):
+        fh.write("# C2 reference-exact (fixed) pair: k_pair_normals_x, then the guarded exact force pass k_pair3<0,0,0,1>\n" + summary(os.path.join(G, "c2_fixed.ncu-rep"), 2))
+    if os.path.exists(os.path.join(G, "band8.ncu-rep")):
+        fh.write("# 8-way band of C5 (516 local rows), self-linked: BAND k_pair3 with peer stores + in-kernel seam handshake\n" + summary(os.path.join(G, "band8.ncu-rep"), 1))
 t = {"_source": f"ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum per launch "
                 f"(profiles/{R}_ncu_summary.txt): C2 / C5_frame = fused k_pair3<1,0>, "
                 "C5 = k_pair3<0,0> force pass, C5_normals = k_pair_normals, C3_detect = the "
@@ -67,8 +71,10 @@ print(json.dumps(t, indent=1))
 
 lib = os.path.join(ROOT, "paper_2507_11794_b200", "_lib", "libclothsim_b200.so")
 sass = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
-want = {"k_pair3ILb1ELb0ELb0": f"{R}_sass_k_pair3_fused.txt",
-        "k_pair3ILb0ELb0ELb0": f"{R}_sass_k_pair3_force.txt",
+want = {"k_pair3ILb1ELb0ELb0ELb0ELb0E": f"{R}_sass_k_pair3_fused.txt",
+        "k_pair3ILb0ELb0ELb0ELb0ELb0E": f"{R}_sass_k_pair3_force.txt",
+        "k_pair3ILb0ELb0ELb0ELb1ELb0E": f"{R}_sass_k_pair3_exact.txt",
+        "k_pair3ILb1ELb0ELb0ELb0ELb1E": f"{R}_sass_k_pair3_band.txt",
         "k_detect_tri": f"{R}_sass_k_detect_tri.txt"}
 for part in sass.split("Function : ")[1:]:
     name = part.split("\n", 1)[0]
