@@ -451,10 +451,13 @@ static void pass_normals(cs_engine *h, cudaStream_t st = nullptr) {
 // frame t runs inside frame t+1's force pass; the buffer is marked stale and
 // refreshed by a stand-alone normals launch only when it is read.
 static void launch_frame(cs_engine *h) {
-    // (A side-stream variant that ran the previous frame's normals
-    // concurrently with this frame's step measured 319.6 vs 321.6 us at
-    // 4096^2 -- both kernels fill the SMs -- and was dropped; retried with
-    // the TMA kernel at C2, where the SMs are not full: 22.6 vs 20.5 us.)
+    // The fast mode fuses the normals into the step kernel.  A side-stream
+    // variant (the starting state's normals beside a force-only step) lost:
+    // 319.6 vs 321.6 us at 4096^2, where both kernels fill the SMs, and
+    // 22.6 vs 20.5 us at C2; on an 8-way band the pieces alone are 26.7 +
+    // 13.3 us against 33.4 us fused (tools/band_split.py).  The exact mode,
+    // whose normals are a separate kernel anyway, does run them beside the
+    // force pass (lag_normals: C2 52.1 -> 51.4 us, C5 813 -> 739 us).
     const bool fuse = h->fuse_normals(), lag = h->lag_normals();
     if (lag) {  // the starting state's normals, beside the force pass
         cudaEventRecord(h->ev_fork, h->st);

@@ -1,3 +1,6 @@
+# A/B of library build variants (tools/ab_build.py; VARS="prev base ...",
+# base = the in-tree library): C2 fast + fixed frames, C5 fast frame and the
+# 8-way band of C5 (plain / stream / in-kernel seam)
 for v in ${VARS:-prev base}; do
   L=$PWD/paper_2507_11794_b200/_lib/var_$v.so; [ $v = base ] && L=$PWD/paper_2507_11794_b200/_lib/libclothsim_b200.so
   echo "== $v"
