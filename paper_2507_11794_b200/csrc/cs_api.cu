@@ -155,6 +155,8 @@ struct cs_engine {
     void *stage = nullptr;
     size_t stage_bytes = 0;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    // graphs of graph_frames frames (CS_GRAPH_FRAMES, even), per start parity
+    cudaGraphExec_t graphG[2] = {nullptr, nullptr};
     // optional contact log (cs_contact_log / cs_read_contacts)
     uint32_t *clog = nullptr, *clog_n = nullptr;
     int64_t clog_cap = 0;
@@ -322,11 +324,33 @@ static int download_planes(cs_engine *h, const T *planes, T *host, int comps) {
 }
 
 static void drop_graphs(cs_engine *h) {
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < 2; ++i) {
         if (h->graph[i]) {
             cudaGraphExecDestroy(h->graph[i]);
             h->graph[i] = nullptr;
         }
+        if (h->graphG[i]) {
+            cudaGraphExecDestroy(h->graphG[i]);
+            h->graphG[i] = nullptr;
+        }
+    }
+}
+
+// frames per captured graph for runs of many frames (CS_GRAPH_FRAMES, an
+// even count so a graph returns to its starting state buffer; 1 = one frame
+// per graph).  Inside a graph consecutive step kernels overlap launch and
+// drain (programmatic dependent launch, CS_PDL in cs_pair3.cu): 8-way band
+// of C5, linked, 34.9 -> 33.8 us per frame with 8 frames per graph; C2 and
+// C5 unchanged (tools/ab_pdl.sh)
+static int graph_frames() {
+    static int g = -1;
+    if (g < 0) {
+        const char *e = getenv("CS_GRAPH_FRAMES");
+        g = e ? atoi(e) : 8;
+        if (g > 1 && (g & 1)) ++g;
+        if (g < 1) g = 1;
+    }
+    return g;
 }
 
 // ---------------------------------------------------------------------------
@@ -1145,29 +1169,34 @@ extern "C" int cs_step(cs_engine *h, int32_t frames) {
         CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&h->ev_nrm, cudaEventDisableTiming));
     }
-    for (int32_t f = 0; f < frames; ++f) {
+    const int G = graph_frames();
+    for (int32_t f = 0; f < frames;) {
+        int n = 1;  // frames this iteration
         if (h->use_graph) {
             const int start = h->cur;
-            if (!h->graph[start]) {
+            n = (G > 1 && frames - f >= G) ? G : 1;
+            cudaGraphExec_t &ge = n > 1 ? h->graphG[start] : h->graph[start];
+            if (!ge) {
                 cudaGraph_t g;
                 CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
-                launch_frame(h);
+                for (int k = 0; k < n; ++k) launch_frame(h);
                 CK(cudaStreamEndCapture(h->st, &g));
-                CK(cudaGraphInstantiate(&h->graph[start], g, 0));
+                CK(cudaGraphInstantiate(&ge, g, 0));
                 cudaGraphDestroy(g);
                 h->cur = start;  // capture did not execute anything
             }
-            CK(cudaGraphLaunch(h->graph[start], h->st));
-            // replay the parity bookkeeping of one frame
-            if (h->substeps & 1) h->cur = 1 - start;
+            CK(cudaGraphLaunch(ge, h->st));
+            // replay the parity bookkeeping of the graph's frames
+            if ((h->substeps * n) & 1) h->cur = 1 - start;
             h->forces_valid = true;
             h->normals_stale = h->normals_lagged();
         } else {
             launch_frame(h);
             CK(cudaGetLastError());
         }
-        if (h->banded) h->passes += (uint32_t)h->substeps;  // replayed in-kernel handshakes
-        h->frames++;
+        if (h->banded) h->passes += (uint32_t)(h->substeps * n);  // replayed in-kernel handshakes
+        h->frames += n;
+        f += n;
     }
     return 0;
 }
