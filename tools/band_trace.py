@@ -81,6 +81,24 @@ if linked:
               f" row loop done {np.median(lp[sel]):.2f}"
               + (f", epilogue done {np.median(ep[sel]):.2f}" if (st[sel, 2] > 0).all() else "")
               + f", signal done {np.median(sg[sel]):.2f} us")
+# does the finish order on a sub-partition follow warp (block) order?
+wid = np.nonzero(buf[:, 1] > 0)[0]
+groups = {}
+for w_, pi, e in zip(wid, part, end):
+    groups.setdefault(int(pi), []).append((int(w_), float(e)))
+same = total = 0
+for g in groups.values():
+    if len(g) == 3:
+        total += 1
+        by_id = [x[0] for x in sorted(g)]
+        by_end = [x[0] for x in sorted(g, key=lambda x: x[1])]
+        same += by_id == by_end
+if total:
+    print(f"  3-warp sub-partitions finishing in warp-id order: {same} of {total}")
+    for rank in range(3):
+        ids = [sorted(g)[rank][0] for g in groups.values() if len(g) == 3]
+        ends_r = [sorted(g)[rank][1] for g in groups.values() if len(g) == 3]
+        print(f"    id rank {rank}: mean warp id {np.mean(ids):7.1f}, mean end {np.mean(ends_r):6.2f} us")
 ends = {}
 for pi, e in zip(part, end):
     ends.setdefault(int(pi), []).append(float(e))
