@@ -102,7 +102,7 @@ __device__ __forceinline__ V3<typename Acc<FIXED>::T> fwd(const N6 &a, const N6 
                                                           bool ok) {
     const float dx = b.x - a.x, dy = b.y - a.y, dz = b.z - a.z;
     const float ux = b.vx - a.vx, uy = b.vy - a.vy, uz = b.vz - a.vz;
-    if (FIXED) {
+    if constexpr (FIXED) {
         int32_t ex, ey, ez;
         spring_fixed(dx, dy, dz, ux, uy, uz, k, rest, c, scale_f, ex, ey, ez);
         if (!ok) ex = ey = ez = 0;
