@@ -414,7 +414,8 @@ __device__ __forceinline__ bool seg_tri(const float *st, const float *en, const 
     const float d0 = fsub(en[0], st[0]), d1 = fsub(en[1], st[1]), d2 = fsub(en[2], st[2]);
     const float d_len = fsqrt(dot3x(d0, d1, d2, d0, d1, d2));
     if (!(d_len > eps)) return false;
-    const float r0 = fdiv(d0, d_len), r1 = fdiv(d1, d_len), r2 = fdiv(d2, d_len);
+    float r0, r1, r2;  // d / |d|: IEEE quotients, one shared reciprocal (div3)
+    div3<true>(d0, d1, d2, d_len, r0, r1, r2);
     const float e10 = fsub(v1[0], v0[0]), e11 = fsub(v1[1], v0[1]), e12 = fsub(v1[2], v0[2]);
     const float e20 = fsub(v2[0], v0[0]), e21 = fsub(v2[1], v0[1]), e22 = fsub(v2[2], v0[2]);
     const float h0 = fsub(fmul(r1, e22), fmul(r2, e21));
