@@ -131,8 +131,12 @@ struct cs_engine {
     bool lag_normals() const {
         if (fuse_normals() || banded || !(grid && strip && fixed && (flags & CS_FLAG_PAIRED)))
             return false;
-        const char *e = getenv("CS_NRM_OVERLAP");
-        return !(e && e[0] == '0');
+        static int on = -1;  // read once
+        if (on < 0) {
+            const char *e = getenv("CS_NRM_OVERLAP");
+            on = !(e && e[0] == '0');
+        }
+        return on != 0;
     }
     bool normals_lagged() const { return fuse_normals() || lag_normals(); }
     cudaStream_t nrm_st = nullptr;
