@@ -389,3 +389,21 @@ def test_fixed_mode_normals_guard_edges():
     from paper_2507_11794_b200 import _native as N
     N.check(eng._lib.cs_run_pass(eng._handle, N.PASS_NORMALS))  # the normals of the written state
     np.testing.assert_array_equal(eng.read_normals(), eo.normals)
+
+
+@pytest.mark.parametrize("precision", ["fast", "fixed"])
+@pytest.mark.parametrize("shape", [(67, 130), (800, 96), (61, 47)])
+def test_multi_frame_graphs_equal_single_frames(precision, shape):
+    """step_frames(n >= 8) replays graphs of 8 frames whose step kernels
+    overlap by programmatic dependent launch (CS_GRAPH_FRAMES, CS_PDL); the
+    state must equal frame-by-frame stepping (one-frame graphs) bit for bit."""
+    params = P.SimParams(dt=0.004)
+    a = P.Engine.from_grid(shape[0], shape[1], params, precision=precision)
+    b = P.Engine.from_grid(shape[0], shape[1], params, precision=precision)
+    a.step_frames(40)  # 5 graphs of 8
+    for _ in range(40):
+        b.step_frames(1)
+    np.testing.assert_array_equal(a.read_positions(), b.read_positions())
+    np.testing.assert_array_equal(a.read_velocities(), b.read_velocities())
+    np.testing.assert_array_equal(a.read_normals(), b.read_normals())
+    assert a.frame_count == b.frame_count == 40
