@@ -241,3 +241,33 @@ def test_bench_gpus_2_under_torchrun_prints_one_banded_line():
     assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
     assert d["config"]["nodes"] == 4096 * 4096 and d["finite"]
     assert {"roofline", "e2e", "gpu_launches", "clocks"} <= set(d)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fixed_bands_guard_rerun_bit_identical(world):
+    """Reference-exact row bands whose springs all leave the exact kernel's
+    guard (k = 1e7: forces far above 2^22 / scale), so every chunk -- seam
+    chunks included, with their peer stores -- is recomputed by the builtin
+    re-run (spring1x_ref); the owned rows still equal one engine bit for
+    bit."""
+    from paper_2507_11794_b200.bands import link_local
+
+    params = P.SimParams(dt=CONTACT_DT, stiffness=1e7, damping=0.5)
+    n = 70
+    whole = P.Engine(P.build_scene(P.ScenarioConfig("hanging", (n, n), dt=CONTACT_DT)).mesh,
+                     params=params, precision="fixed")
+    bands = [BandedEngine(n, n, params, r, world, exchange="p2p", precision="fixed")
+             for r in range(world)]
+    link_local(bands)
+    whole.step_frames(6)
+    for _ in range(6):
+        for b in bands:
+            b.step(1)
+        for b in bands:
+            b.engine.synchronize()
+    for what in ("positions", "velocities", "normals"):
+        got = np.concatenate([getattr(b, f"owned_{what}")() for b in bands])
+        np.testing.assert_array_equal(got, getattr(whole, f"read_{what}")(), err_msg=what)
+    assert np.abs(whole.read_forces_raw()).max() > (1 << 22)  # the guard really failed
+    for b in bands:
+        b.close()
