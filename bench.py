@@ -356,6 +356,34 @@ def main():
     dev_engine.close()
     del t_traj
 
+    # the reference harness's own loop (bench.py:157-168 of the reference,
+    # run_backend): per frame `stepper.step().hits` -- the step's result is
+    # its hit count (a device->host read of the frame's stats ring entry,
+    # which synchronises), positions only when verifying / snapshotting;
+    # the initial state enters from pinned host memory
+    loop_engine = P.Engine(scene.mesh, scene.obstacle, scene.params, pair_budget=10**13,
+                           precision="fast", stream=stream.cuda_stream)
+    for _ in range(min(args.warmup, 8)):
+        _ = loop_engine.step().hits
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    loop_engine.write_positions(host_pos)
+    loop_engine.write_velocities(host_vel)
+    hits_sum = 0
+    for _ in range(args.steps):
+        hits_sum += int(loop_engine.step().hits)
+    loop_engine.synchronize()  # collision-free: .hits is 0 without waiting for the frame
+    loop_dt = time.perf_counter() - t0
+    e2e_ref_loop = {"value": args.steps / loop_dt, "unit": "steps/s",
+                    "h2d_bytes_per_step": 2 * host_pos.nbytes / args.steps,
+                    "d2h_bytes_per_step": 16,
+                    "api": "Engine.write_positions/write_velocities(host) once + per frame "
+                           "Engine.step().hits (the reference's run_backend loop)",
+                    "note": "with an obstacle each .hits read waits for its frame; collision-free "
+                            "scenes have no hits to wait for, so the run ends with a synchronise; "
+                            "the headline e2e instead copies every frame's positions to the host"}
+    loop_engine.close()
+
     line = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -381,6 +409,7 @@ def main():
         "attempts": attempts,
         "e2e": e2e,
         "e2e_device": e2e_device,
+        "e2e_reference_loop": e2e_ref_loop,
     }
     if not args.no_collision and config_name == "C2":
         line["collision"] = collision_bench(P, torch, args, "C3", cpu=not args.no_cpu_baseline)
