@@ -148,7 +148,8 @@ def test_c3_drapes_finite_with_contacts_in_both_modes():
     (2, "fast", 160, "auto", "kernel"), (3, "fast", 161, "auto", "kernel"),
     (3, "fast", 130, "split", "kernel"), (4, "fixed", 96, "auto", "kernel"),
     (2, "fast", 64, "fused", "kernel"), (3, "fast", 161, "auto", "stream"),
-    (4, "fast", 300, "auto", "kernel"),
+    (4, "fast", 300, "auto", "kernel"), (8, "fast", 300, "auto", "kernel"),
+    (8, "fast", 97, "auto", "kernel"), (8, "fixed", 140, "auto", "kernel"),
 ])
 def test_p2p_bands_bit_identical_to_one_engine(world, precision, n, normals, seam):
     """Row bands linked by peer stores inside the step kernel (the NVLink
