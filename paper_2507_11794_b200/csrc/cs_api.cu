@@ -1009,7 +1009,10 @@ static int build(cs_engine *h, const cs_desc *d, const GridGen *gen = nullptr) {
 
 extern "C" int cs_destroy(cs_engine *h) {
     if (!h) return 0;
+    // every stream that may still touch the engine's buffers, before freeing
     if (h->st) cudaStreamSynchronize(h->st);
+    if (h->nrm_st) cudaStreamSynchronize(h->nrm_st);
+    if (h->copy_st) cudaStreamSynchronize(h->copy_st);
     drop_graphs(h);
     void *ptrs[] = {h->state[0], h->state[1], h->normals, h->pinbits, h->inv_mass, h->mass64,
                     h->pinned8, h->ext, h->forces_raw, h->csr_off, h->csr_nbr, h->csr_kind,
