@@ -407,3 +407,19 @@ def test_multi_frame_graphs_equal_single_frames(precision, shape):
     np.testing.assert_array_equal(a.read_velocities(), b.read_velocities())
     np.testing.assert_array_equal(a.read_normals(), b.read_normals())
     assert a.frame_count == b.frame_count == 40
+
+
+@pytest.mark.parametrize("shape", [(67, 130), (800, 96)])
+def test_fast_eager_launches_equal_graph_replay(shape):
+    """graph=False launches the fused step kernel eagerly -- still with
+    programmatic dependent launch between consecutive frames -- and must
+    equal graph replay (8-frame graphs) bit for bit."""
+    params = P.SimParams(dt=0.004)
+    a = P.Engine.from_grid(shape[0], shape[1], params)
+    b = P.Engine.from_grid(shape[0], shape[1], params, graph=False)
+    a.step_frames(24)
+    b.step_frames(24)
+    for x, y in [(a.read_positions(), b.read_positions()),
+                 (a.read_velocities(), b.read_velocities()),
+                 (a.read_normals(), b.read_normals())]:
+        np.testing.assert_array_equal(x, y)
